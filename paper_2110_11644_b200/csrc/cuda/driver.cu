@@ -1,0 +1,801 @@
+// Host driver of libvsdock.so: implements include/vs_dock.h.
+//
+// Owns contexts (device + stream + reusable device buffers), device-resident
+// pockets (grid + protein + chem culling cells) and the batch pipeline
+//   H2D batch -> k_setup -> k_flatten -> k_search -> k_select -> D2H results
+// processed in chunks that bound the per-restart scratch.  Input-independent
+// trig (Fibonacci restarts, rotation spins: search.cpp:71-82, 97-98, 162-163)
+// is computed here once per call with glibc, exactly as the reference does,
+// and shipped to the device as tables.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../../include/vs_crtrig.h"
+#include "../../../include/vs_dock.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+vs_status fail(vs_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(VS_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <typename T>
+  T *as() const {
+    return static_cast<T *>(p);
+  }
+};
+
+constexpr double kPi = 3.14159265358979323846;
+std::once_flag g_lattice_once[64];
+
+}  // namespace
+
+struct vs_context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int last_launches = 0;
+  std::mutex mu;
+  // batch inputs
+  DevBuf atom_off, bond_off, tors_off, ditem_base, xyz, elem, heavy, bond_a, bond_b, tors_bond, right_off, right_atoms;
+  // derived
+  DevBuf meta, tmask, heavy_list, dmask, tors_ha, tors_hb, d_count, d_off, ditems;
+  // flatten / search / select
+  DevBuf flat_idx, flat_xyz, flat_centroid, out_geo, out_T, out_ang, out_conf, out_evals, out_status, work;
+  DevBuf results, best_ang, best_conf, spin, fibq;
+  DevBuf aux0, aux1, aux2, aux3;
+};
+
+struct vs_pocket {
+  int device = 0;
+  double origin[3] = {0, 0, 0};
+  double spacing = 0.5;
+  int dims[3] = {0, 0, 0};
+  int n_protein = 0;
+  DevBuf values, pxyz, pclass, cell_start, cell_atoms;
+  double cmin[3] = {0, 0, 0};
+  double cs = 2.0;
+  int cdims[3] = {0, 0, 0};
+  bool has_cells = false;
+
+  vsd::pocket_dev dev() const {
+    vsd::pocket_dev p{};
+    p.g.ox = origin[0];
+    p.g.oy = origin[1];
+    p.g.oz = origin[2];
+    p.g.h = spacing;
+    p.g.mx = static_cast<double>(dims[0] - 1);
+    p.g.my = static_cast<double>(dims[1] - 1);
+    p.g.mz = static_cast<double>(dims[2] - 1);
+    p.g.dx = dims[0];
+    p.g.dy = dims[1];
+    p.g.dz = dims[2];
+    p.g.v = values.as<double>();
+    const double hs = 0.5 * spacing;  // box_center, pocket.hpp:53-56
+    for (int a = 0; a < 3; ++a) p.center[a] = origin[a] + hs * static_cast<double>(dims[a] - 1);
+    p.n_protein = n_protein;
+    p.pxyz = pxyz.as<double>();
+    p.pclass = pclass.as<uint8_t>();
+    for (int a = 0; a < 3; ++a) {
+      p.cmin[a] = cmin[a];
+      p.cdims[a] = cdims[a];
+    }
+    p.cs = cs;
+    p.cell_start = has_cells ? cell_start.as<int>() : nullptr;
+    p.cell_atoms = has_cells ? cell_atoms.as<int>() : nullptr;
+    return p;
+  }
+};
+
+namespace {
+
+void ensure_lattice(int device) {
+  std::call_once(g_lattice_once[device & 63], [] {
+    double sc[72];
+    constexpr double step = 2.0 * kPi / 36;  // search.cpp:33
+    for (int i = 0; i < 36; ++i) vs_crtrig::sincos_cr(i * step, &sc[2 * i], &sc[2 * i + 1]);
+    vsd::set_lattice_table(sc);
+  });
+}
+
+int chem_class(uint8_t e) { return e == VS_ELEM_C ? 0 : ((e == VS_ELEM_N || e == VS_ELEM_O) ? 1 : 2); }
+
+// Culling cells for chem_score: every protein atom whose distance to the
+// cell's box is below 4.5 A (+1e-6 margin), listed in protein order.
+vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
+  const double cutoff = 4.5 + 1e-6;
+  const double cs = 2.0;
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = p->origin[a] - 5.0;
+    hi[a] = p->origin[a] + p->spacing * (p->dims[a] - 1) + 5.0;
+    p->cdims[a] = static_cast<int>(std::ceil((hi[a] - lo[a]) / cs));
+    p->cmin[a] = lo[a];
+  }
+  p->cs = cs;
+  const int64_t ncell = static_cast<int64_t>(p->cdims[0]) * p->cdims[1] * p->cdims[2];
+  if (ncell <= 0 || ncell > (1 << 22) || p->n_protein == 0) {
+    p->has_cells = false;
+    return VS_OK;
+  }
+  std::vector<std::vector<int>> lists(static_cast<size_t>(ncell));
+  const int reach = static_cast<int>(std::ceil(cutoff / cs)) + 1;
+  for (int j = 0; j < p->n_protein; ++j) {
+    const double x[3] = {xyz[3 * j], xyz[3 * j + 1], xyz[3 * j + 2]};
+    int c[3];
+    for (int a = 0; a < 3; ++a) c[a] = static_cast<int>(std::floor((x[a] - lo[a]) / cs));
+    for (int dz = -reach; dz <= reach; ++dz)
+      for (int dy = -reach; dy <= reach; ++dy)
+        for (int dx = -reach; dx <= reach; ++dx) {
+          const int cc[3] = {c[0] + dx, c[1] + dy, c[2] + dz};
+          if (cc[0] < 0 || cc[1] < 0 || cc[2] < 0 || cc[0] >= p->cdims[0] || cc[1] >= p->cdims[1] ||
+              cc[2] >= p->cdims[2])
+            continue;
+          double d2 = 0.0;
+          for (int a = 0; a < 3; ++a) {
+            const double bl = lo[a] + cc[a] * cs, bh = bl + cs;
+            const double q = x[a] < bl ? bl - x[a] : (x[a] > bh ? x[a] - bh : 0.0);
+            d2 += q * q;
+          }
+          if (d2 < cutoff * cutoff)
+            lists[static_cast<size_t>(cc[0] + p->cdims[0] * (cc[1] + static_cast<int64_t>(p->cdims[1]) * cc[2]))]
+                .push_back(j);
+        }
+  }
+  (void)elem;
+  std::vector<int> start(static_cast<size_t>(ncell) + 1, 0), atoms;
+  for (int64_t c = 0; c < ncell; ++c) {
+    start[static_cast<size_t>(c)] = static_cast<int>(atoms.size());
+    atoms.insert(atoms.end(), lists[static_cast<size_t>(c)].begin(), lists[static_cast<size_t>(c)].end());
+  }
+  start[static_cast<size_t>(ncell)] = static_cast<int>(atoms.size());
+  if (atoms.empty()) atoms.push_back(0);
+  CUDA_TRY(p->cell_start.ensure(start.size() * sizeof(int)));
+  CUDA_TRY(p->cell_atoms.ensure(atoms.size() * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(p->cell_start.p, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->cell_atoms.p, atoms.data(), atoms.size() * sizeof(int), cudaMemcpyHostToDevice));
+  p->has_cells = true;
+  return VS_OK;
+}
+
+vs_status upload_protein(vs_pocket *p, int32_t n, const uint8_t *elem, const double *xyz) {
+  p->n_protein = n;
+  std::vector<uint8_t> cls(static_cast<size_t>(std::max(n, 1)), 2);
+  for (int j = 0; j < n; ++j) cls[static_cast<size_t>(j)] = static_cast<uint8_t>(chem_class(elem[j]));
+  CUDA_TRY(p->pxyz.ensure(sizeof(double) * 3 * std::max(n, 1)));
+  CUDA_TRY(p->pclass.ensure(std::max(n, 1)));
+  if (n > 0) {
+    CUDA_TRY(cudaMemcpy(p->pxyz.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(p->pclass.p, cls.data(), static_cast<size_t>(n), cudaMemcpyHostToDevice));
+  }
+  return build_cells(p, elem, xyz);
+}
+
+// One chunk of a ligand batch staged on the device.
+struct Staged {
+  vsd::batch_dev b{};
+  int n = 0;
+  int Nmax = 0, nmax = 0, mmax = 0;
+  int atoms = 0, torsions = 0;
+  std::vector<int> atom_off, bond_off, tors_off, right_off, ditem_base;
+};
+
+template <typename T>
+vs_status h2d(DevBuf &buf, const T *src, size_t count, cudaStream_t s) {
+  CUDA_TRY(buf.ensure(sizeof(T) * std::max<size_t>(count, 1)));
+  if (count) CUDA_TRY(cudaMemcpyAsync(buf.p, src, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  return VS_OK;
+}
+
+// Stage ligands [l0, l1) of `in` (offsets rebased to 0).
+vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Staged &st) {
+  const int n = l1 - l0;
+  st.n = n;
+  const int A0 = in->atom_offset[l0], A1 = in->atom_offset[l1];
+  const int B0 = in->bond_offset[l0], B1 = in->bond_offset[l1];
+  const int T0 = in->torsion_offset[l0], T1 = in->torsion_offset[l1];
+  const int R0 = in->right_offset[T0], R1 = in->right_offset[T1];
+  st.atoms = A1 - A0;
+  st.torsions = T1 - T0;
+  st.atom_off.resize(n + 1);
+  st.bond_off.resize(n + 1);
+  st.tors_off.resize(n + 1);
+  st.ditem_base.resize(n + 1);
+  st.right_off.resize(T1 - T0 + 1);
+  st.Nmax = st.nmax = st.mmax = 0;
+  int dbase = 0;
+  for (int i = 0; i <= n; ++i) {
+    st.atom_off[i] = in->atom_offset[l0 + i] - A0;
+    st.bond_off[i] = in->bond_offset[l0 + i] - B0;
+    st.tors_off[i] = in->torsion_offset[l0 + i] - T0;
+    st.ditem_base[i] = dbase;
+    if (i < n) {
+      const int N = in->atom_offset[l0 + i + 1] - in->atom_offset[l0 + i];
+      const int m = in->torsion_offset[l0 + i + 1] - in->torsion_offset[l0 + i];
+      int h = 0;
+      for (int a = in->atom_offset[l0 + i]; a < in->atom_offset[l0 + i + 1]; ++a) h += in->is_heavy[a] ? 1 : 0;
+      if (N <= VS_MAX_ATOMS && m <= VS_MAX_TORSIONS && h <= VS_MAX_HEAVY) {
+        st.Nmax = std::max(st.Nmax, N);
+        st.mmax = std::max(st.mmax, m);
+        st.nmax = std::max(st.nmax, h);
+      }
+      dbase += std::min(m, VS_MAX_TORSIONS) * std::min(N, VS_MAX_ATOMS);
+    }
+  }
+  for (int t = 0; t <= T1 - T0; ++t) st.right_off[t] = in->right_offset[T0 + t] - R0;
+  cudaStream_t s = ctx->stream;
+  vs_status rc;
+  if ((rc = h2d(ctx->atom_off, st.atom_off.data(), n + 1, s))) return rc;
+  if ((rc = h2d(ctx->bond_off, st.bond_off.data(), n + 1, s))) return rc;
+  if ((rc = h2d(ctx->tors_off, st.tors_off.data(), n + 1, s))) return rc;
+  if ((rc = h2d(ctx->ditem_base, st.ditem_base.data(), n + 1, s))) return rc;
+  if ((rc = h2d(ctx->right_off, st.right_off.data(), T1 - T0 + 1, s))) return rc;
+  if ((rc = h2d(ctx->xyz, in->xyz + 3 * static_cast<size_t>(A0), 3 * static_cast<size_t>(A1 - A0), s))) return rc;
+  if ((rc = h2d(ctx->elem, in->element + A0, A1 - A0, s))) return rc;
+  if ((rc = h2d(ctx->heavy, in->is_heavy + A0, A1 - A0, s))) return rc;
+  if ((rc = h2d(ctx->bond_a, in->bond_a + B0, B1 - B0, s))) return rc;
+  if ((rc = h2d(ctx->bond_b, in->bond_b + B0, B1 - B0, s))) return rc;
+  if ((rc = h2d(ctx->tors_bond, in->torsion_bond + T0, T1 - T0, s))) return rc;
+  if ((rc = h2d(ctx->right_atoms, in->right_atoms + R0, R1 - R0, s))) return rc;
+  const size_t na = std::max(st.atoms, 1), nt = std::max(st.torsions, 1);
+  CUDA_TRY(ctx->meta.ensure(sizeof(vsd::lig_meta) * std::max(n, 1)));
+  CUDA_TRY(ctx->tmask.ensure(4 * na));
+  CUDA_TRY(ctx->heavy_list.ensure(2 * na));
+  CUDA_TRY(ctx->dmask.ensure(4 * na));
+  CUDA_TRY(ctx->tors_ha.ensure(2 * nt));
+  CUDA_TRY(ctx->tors_hb.ensure(2 * nt));
+  CUDA_TRY(ctx->d_count.ensure(4 * nt));
+  CUDA_TRY(ctx->d_off.ensure(4 * nt));
+  CUDA_TRY(ctx->ditems.ensure(2 * static_cast<size_t>(std::max(dbase, 1))));
+  vsd::batch_dev &b = st.b;
+  b.n_lig = n;
+  b.atom_off = ctx->atom_off.as<int>();
+  b.bond_off = ctx->bond_off.as<int>();
+  b.tors_off = ctx->tors_off.as<int>();
+  b.ditem_base = ctx->ditem_base.as<int>();
+  b.xyz = ctx->xyz.as<double>();
+  b.elem = ctx->elem.as<uint8_t>();
+  b.heavy = ctx->heavy.as<uint8_t>();
+  b.bond_a = ctx->bond_a.as<uint16_t>();
+  b.bond_b = ctx->bond_b.as<uint16_t>();
+  b.tors_bond = ctx->tors_bond.as<uint16_t>();
+  b.right_off = ctx->right_off.as<int>();
+  b.right_atoms = ctx->right_atoms.as<uint16_t>();
+  b.meta = ctx->meta.as<vsd::lig_meta>();
+  b.atom_tmask = ctx->tmask.as<uint32_t>();
+  b.heavy_list = ctx->heavy_list.as<uint16_t>();
+  b.heavy_dmask = ctx->dmask.as<uint32_t>();
+  b.tors_ha = ctx->tors_ha.as<uint16_t>();
+  b.tors_hb = ctx->tors_hb.as<uint16_t>();
+  b.d_count = ctx->d_count.as<int>();
+  b.d_off = ctx->d_off.as<int>();
+  b.ditems = ctx->ditems.as<uint16_t>();
+  return VS_OK;
+}
+
+// Host tables of input-independent rotations (glibc trig, as the reference).
+// spin: per step level L (step_rotation halved L times, search.cpp:188),
+// per neighbour (axis x/y/z, sign +/-), Quaterniond(AngleAxisd(sign*step,
+// Unit(axis))) (search.cpp:162-163, Appendix A item 1).
+int spin_levels(const vs_scoring_config &c) {
+  int levels = 0;
+  double st = c.step_translation;
+  while (levels < c.max_iterations && st >= c.min_translation && levels < 4096) {
+    st *= 0.5;
+    ++levels;
+  }
+  return std::max(levels, 1);
+}
+void spin_table(const vs_scoring_config &c, int levels, std::vector<double> &out) {
+  out.assign(static_cast<size_t>(levels) * 6 * 4, 0.0);
+  double step_r = c.step_rotation;
+  for (int L = 0; L < levels; ++L) {
+    for (int axis = 0; axis < 3; ++axis)
+      for (int sgn = 0; sgn < 2; ++sgn) {
+        const double sign = sgn ? -1.0 : 1.0;
+        const double ha = 0.5 * (sign * step_r);
+        const double w = std::cos(ha), s = std::sin(ha);
+        const double u[3] = {axis == 0 ? 1.0 : 0.0, axis == 1 ? 1.0 : 0.0, axis == 2 ? 1.0 : 0.0};
+        double *q = &out[(static_cast<size_t>(L) * 6 + axis * 2 + sgn) * 4];
+        q[0] = s * u[0];
+        q[1] = s * u[1];
+        q[2] = s * u[2];
+        q[3] = w;
+      }
+    step_r *= 0.5;
+  }
+}
+// fibonacci_axis / fibonacci_rotation_angle / Quaterniond(AngleAxisd)
+// (search.cpp:71-82, 97-98).
+void fib_table(int k, std::vector<double> &out) {
+  constexpr double kGoldenRatio = 1.6180339887498948482;
+  constexpr double kGoldenAngle = 2.0 * kPi * (2.0 - kGoldenRatio);
+  out.assign(static_cast<size_t>(k) * 4, 0.0);
+  for (int i = 0; i < k; ++i) {
+    const double z = 1.0 - 2.0 * (i + 0.5) / static_cast<double>(k);
+    const double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+    const double az = std::fmod(i * kGoldenAngle, 2.0 * kPi);
+    const double ax[3] = {r * std::cos(az), r * std::sin(az), z};
+    const double angle = 2.0 * kPi * std::fmod(i * kGoldenRatio, 1.0);
+    const double ha = 0.5 * angle;
+    const double w = std::cos(ha), s = std::sin(ha);
+    out[4 * i] = s * ax[0];
+    out[4 * i + 1] = s * ax[1];
+    out[4 * i + 2] = s * ax[2];
+    out[4 * i + 3] = w;
+  }
+}
+
+vs_status check_cfg(const vs_scoring_config *cfg) {
+  if (!cfg) return fail(VS_ERR_INVALID_ARGUMENT, "null scoring config");
+  if (cfg->restarts < 1) return fail(VS_ERR_INVALID_ARGUMENT, "restarts must be at least 1");
+  if (cfg->rescored < 1) return fail(VS_ERR_INVALID_ARGUMENT, "rescored must be at least 1");
+  if (!(cfg->rmsd_threshold > 0.0)) return fail(VS_ERR_INVALID_ARGUMENT, "rmsd threshold must be positive");
+  if (cfg->restarts > VS_MAX_RESTARTS) return fail(VS_ERR_LIMIT, "restarts exceed VS_MAX_RESTARTS");
+  return VS_OK;
+}
+
+vs_status upload_tables(vs_context *ctx, const vs_scoring_config &c, int k, vsd::search_cfg &sc) {
+  std::vector<double> spin, fib;
+  const int levels = spin_levels(c);
+  spin_table(c, levels, spin);
+  fib_table(k, fib);
+  vs_status rc;
+  if ((rc = h2d(ctx->spin, spin.data(), spin.size(), ctx->stream))) return rc;
+  if ((rc = h2d(ctx->fibq, fib.data(), fib.size(), ctx->stream))) return rc;
+  sc.k = k;
+  sc.rescored = c.rescored;
+  sc.rmsd_threshold = c.rmsd_threshold;
+  sc.max_iter = c.max_iterations;
+  sc.step_t = c.step_translation;
+  sc.step_r = c.step_rotation;
+  sc.step_q = c.step_torsion;
+  sc.min_t = c.min_translation;
+  sc.flatten_sweeps = c.flatten_max_sweeps;
+  sc.n_levels = levels;
+  sc.spin = ctx->spin.as<double>();
+  sc.fibq = ctx->fibq.as<double>();
+  // The stream must not outlive the host vectors' copies.
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return VS_OK;
+}
+
+// Chunk boundaries so that the per-restart conformation scratch stays under
+// `budget` bytes.
+std::vector<int> chunks(const vs_ligand_batch *b, int k, size_t budget) {
+  std::vector<int> cut{0};
+  size_t acc = 0;
+  for (int i = 0; i < b->n_ligands; ++i) {
+    const size_t N = static_cast<size_t>(b->atom_offset[i + 1] - b->atom_offset[i]);
+    const size_t need = N * k * 3 * sizeof(double) + 256 * static_cast<size_t>(k);
+    if (acc + need > budget && i > cut.back()) {
+      cut.push_back(i);
+      acc = 0;
+    }
+    acc += need;
+  }
+  cut.push_back(b->n_ligands);
+  return cut;
+}
+
+vs_status ensure_items(vs_context *ctx, const Staged &st, int k, vsd::item_out &o) {
+  const size_t items = static_cast<size_t>(std::max(st.n, 1)) * k;
+  CUDA_TRY(ctx->out_geo.ensure(sizeof(double) * items));
+  CUDA_TRY(ctx->out_T.ensure(sizeof(double) * 7 * items));
+  CUDA_TRY(ctx->out_ang.ensure(sizeof(double) * std::max<size_t>(1, static_cast<size_t>(st.torsions) * k)));
+  CUDA_TRY(ctx->out_conf.ensure(sizeof(double) * 3 * std::max<size_t>(1, static_cast<size_t>(st.atoms) * k)));
+  CUDA_TRY(ctx->out_evals.ensure(sizeof(unsigned long long) * items));
+  CUDA_TRY(ctx->out_status.ensure(sizeof(int) * items));
+  CUDA_TRY(ctx->work.ensure(sizeof(int) * 4));
+  o.geo = ctx->out_geo.as<double>();
+  o.T = ctx->out_T.as<double>();
+  o.ang = ctx->out_ang.as<double>();
+  o.conf = ctx->out_conf.as<double>();
+  o.evals = ctx->out_evals.as<unsigned long long>();
+  o.status = ctx->out_status.as<int>();
+  return VS_OK;
+}
+
+vs_status ensure_flat(vs_context *ctx, const Staged &st, vsd::flat_out &f) {
+  CUDA_TRY(ctx->flat_idx.ensure(sizeof(int) * std::max(st.torsions, 1)));
+  CUDA_TRY(ctx->flat_xyz.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
+  CUDA_TRY(ctx->flat_centroid.ensure(sizeof(double) * 3 * std::max(st.n, 1)));
+  f.idx = ctx->flat_idx.as<int>();
+  f.xyz = ctx->flat_xyz.as<double>();
+  f.centroid = ctx->flat_centroid.as<double>();
+  return VS_OK;
+}
+
+struct CtxLock {
+  vs_context *c;
+  explicit CtxLock(vs_context *ctx) : c(ctx) {
+    c->mu.lock();
+    cudaSetDevice(c->device);
+  }
+  ~CtxLock() { c->mu.unlock(); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int vs_abi_version(void) { return VS_ABI_VERSION; }
+
+int vs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char *vs_last_error_message(void) { return g_err.c_str(); }
+
+void vs_scoring_config_default(vs_scoring_config *c) {
+  c->restarts = 256;
+  c->rescored = 30;
+  c->rmsd_threshold = 3.0;
+  c->step_translation = 1.0;
+  c->step_rotation = 20.0 * (kPi / 180.0);
+  c->step_torsion = 20.0 * (kPi / 180.0);
+  c->min_translation = 0.1;
+  c->max_iterations = 200;
+  c->flatten_max_sweeps = 20;
+}
+
+vs_status vs_context_create(int device, vs_context **out) {
+  if (!out) return fail(VS_ERR_INVALID_ARGUMENT, "null output");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(VS_ERR_NO_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(VS_ERR_INVALID_ARGUMENT, "device index out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10) return fail(VS_ERR_NO_DEVICE, "libvsdock is built for sm_100a (B200) only");
+  auto *ctx = new vs_context;
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return fail(VS_ERR_CUDA, "stream creation failed");
+  }
+  cudaEventCreate(&ctx->ev0);
+  cudaEventCreate(&ctx->ev1);
+  ensure_lattice(device);
+  *out = ctx;
+  return VS_OK;
+}
+
+vs_status vs_context_destroy(vs_context *ctx) {
+  if (!ctx) return VS_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return VS_OK;
+}
+
+vs_status vs_context_last_timing(vs_context *ctx, double *kernel_ms, int32_t *launches) {
+  if (!ctx) return fail(VS_ERR_INVALID_ARGUMENT, "null context");
+  if (kernel_ms) *kernel_ms = ctx->last_ms;
+  if (launches) *launches = ctx->last_launches;
+  return VS_OK;
+}
+
+vs_status vs_pocket_create(vs_context *ctx, const vs_pocket_desc *d, vs_pocket **out) {
+  if (!ctx || !d || !out) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  for (int a = 0; a < 3; ++a)
+    if (d->dims[a] < 2) return fail(VS_ERR_INVALID_ARGUMENT, "every pocket dimension must be at least 2");
+  if (!(d->spacing > 0.0)) return fail(VS_ERR_INVALID_ARGUMENT, "pocket spacing must be positive");
+  CtxLock lock(ctx);
+  auto *p = new vs_pocket;
+  p->device = ctx->device;
+  for (int a = 0; a < 3; ++a) {
+    p->origin[a] = d->origin[a];
+    p->dims[a] = d->dims[a];
+  }
+  p->spacing = d->spacing;
+  const size_t nv = static_cast<size_t>(d->dims[0]) * d->dims[1] * d->dims[2];
+  vs_status rc = VS_OK;
+  if (p->values.ensure(sizeof(double) * nv) != cudaSuccess ||
+      cudaMemcpy(p->values.p, d->values, sizeof(double) * nv, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(VS_ERR_CUDA, "pocket grid upload failed");
+  if (rc == VS_OK) rc = upload_protein(p, d->n_protein, d->protein_element, d->protein_xyz);
+  if (rc != VS_OK) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return VS_OK;
+}
+
+vs_status vs_pocket_build(vs_context *ctx, int32_t n, const uint8_t *elem, const double *xyz, const double center[3],
+                          double radius, double spacing, vs_pocket **out) {
+  if (!ctx || !out || !center) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  // Preconditions of build_pocket (grid.cpp:18-25).
+  if (radius <= 0.0) return fail(VS_ERR_INVALID_ARGUMENT, "pocket radius must be positive");
+  if (spacing < 0.25 || spacing > 1.0) return fail(VS_ERR_INVALID_ARGUMENT, "pocket spacing must lie in [0.25, 1.0]");
+  std::vector<double> heavy;
+  for (int j = 0; j < n; ++j)
+    if (elem[j] != VS_ELEM_H) heavy.insert(heavy.end(), xyz + 3 * j, xyz + 3 * j + 3);
+  if (heavy.empty()) return fail(VS_ERR_INVALID_ARGUMENT, "protein has no heavy atoms");
+  const int steps = static_cast<int>(std::ceil(2.0 * radius / spacing));
+  const int dim = steps + 1;
+  if (static_cast<int64_t>(dim) * dim * dim > (int64_t(1) << 27)) return fail(VS_ERR_LIMIT, "pocket grid too large");
+  CtxLock lock(ctx);
+  auto *p = new vs_pocket;
+  p->device = ctx->device;
+  p->spacing = spacing;
+  for (int a = 0; a < 3; ++a) {
+    p->origin[a] = center[a] - radius;  // center - Constant(radius)
+    p->dims[a] = dim;
+  }
+  const size_t nv = static_cast<size_t>(dim) * dim * dim;
+  DevBuf hx;
+  vs_status rc = VS_OK;
+  if (p->values.ensure(sizeof(double) * nv) != cudaSuccess || hx.ensure(sizeof(double) * heavy.size()) != cudaSuccess ||
+      cudaMemcpy(hx.p, heavy.data(), sizeof(double) * heavy.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(VS_ERR_CUDA, "pocket build upload failed");
+  if (rc == VS_OK) {
+    cudaError_t e = vsd::launch_build_pocket(hx.as<double>(), static_cast<int>(heavy.size() / 3), center[0], center[1],
+                                             center[2], radius, p->origin[0], p->origin[1], p->origin[2], spacing, dim,
+                                             dim, dim, p->values.as<double>(), ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(VS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (rc == VS_OK) rc = upload_protein(p, n, elem, xyz);
+  if (rc != VS_OK) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return VS_OK;
+}
+
+vs_status vs_pocket_info(const vs_pocket *p, double origin[3], double *spacing, int32_t dims[3], int32_t *n_protein) {
+  if (!p) return fail(VS_ERR_INVALID_ARGUMENT, "null pocket");
+  for (int a = 0; a < 3; ++a) {
+    if (origin) origin[a] = p->origin[a];
+    if (dims) dims[a] = p->dims[a];
+  }
+  if (spacing) *spacing = p->spacing;
+  if (n_protein) *n_protein = p->n_protein;
+  return VS_OK;
+}
+
+vs_status vs_pocket_download(vs_context *ctx, const vs_pocket *p, double *values) {
+  if (!ctx || !p || !values) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  const size_t nv = static_cast<size_t>(p->dims[0]) * p->dims[1] * p->dims[2];
+  CUDA_TRY(cudaMemcpy(values, p->values.p, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+  return VS_OK;
+}
+
+vs_status vs_pocket_destroy(vs_pocket *p) {
+  if (!p) return VS_OK;
+  cudaSetDevice(p->device);
+  delete p;
+  return VS_OK;
+}
+
+vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                        const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
+                        double *best_conformation) {
+  if (!ctx || !pocket || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  vs_status rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (pocket->device != ctx->device) return fail(VS_ERR_INVALID_ARGUMENT, "pocket lives on another device");
+  CtxLock lock(ctx);
+  const int k = cfg->restarts;
+  vsd::search_cfg sc{};
+  if ((rc = upload_tables(ctx, *cfg, k, sc))) return rc;
+  const vsd::pocket_dev pd = pocket->dev();
+  ctx->last_launches = 0;
+  float total_ms = 0.0f;
+  const std::vector<int> cut = chunks(batch, k, size_t(3) << 30);
+  for (size_t ci = 0; ci + 1 < cut.size(); ++ci) {
+    const int l0 = cut[ci], l1 = cut[ci + 1];
+    Staged st;
+    if ((rc = stage(ctx, batch, l0, l1, st))) return rc;
+    vsd::flat_out f{};
+    vsd::item_out o{};
+    if ((rc = ensure_flat(ctx, st, f))) return rc;
+    if ((rc = ensure_items(ctx, st, k, o))) return rc;
+    CUDA_TRY(ctx->results.ensure(sizeof(vs_dock_result) * std::max(st.n, 1)));
+    CUDA_TRY(ctx->best_ang.ensure(sizeof(double) * std::max(st.torsions, 1)));
+    CUDA_TRY(ctx->best_conf.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
+    vsd::dock_out d{ctx->results.p, ctx->best_ang.as<double>(), ctx->best_conf.as<double>()};
+    CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(vsd::launch_setup(st.b, k, ctx->stream));
+    CUDA_TRY(vsd::launch_flatten(st.b, cfg->flatten_max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
+    CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax, ctx->num_sms,
+                                ctx->stream, nullptr));
+    CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->last_launches += 4;
+    CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    const int T0 = batch->torsion_offset[l0], A0 = batch->atom_offset[l0];
+    if (best_angles && st.torsions)
+      CUDA_TRY(cudaMemcpyAsync(best_angles + T0, ctx->best_ang.p, sizeof(double) * st.torsions, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    if (best_conformation && st.atoms)
+      CUDA_TRY(cudaMemcpyAsync(best_conformation + 3 * static_cast<size_t>(A0), ctx->best_conf.p,
+                               sizeof(double) * 3 * st.atoms, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    total_ms += ms;
+  }
+  ctx->last_ms = total_ms;
+  return VS_OK;
+}
+
+vs_status vs_field_values(vs_context *ctx, const vs_pocket *pocket, int64_t n, const double *xyz, double *out) {
+  if (!ctx || !pocket || (n > 0 && (!xyz || !out))) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  vs_status rc;
+  if ((rc = h2d(ctx->aux0, xyz, 3 * static_cast<size_t>(n), ctx->stream))) return rc;
+  CUDA_TRY(ctx->aux1.ensure(sizeof(double) * std::max<int64_t>(n, 1)));
+  CUDA_TRY(vsd::launch_field_values(pocket->dev(), n, ctx->aux0.as<double>(), ctx->aux1.as<double>(), ctx->stream));
+  if (n) CUDA_TRY(cudaMemcpyAsync(out, ctx->aux1.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return VS_OK;
+}
+
+vs_status vs_geo_score_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                             const double *conformation, double *out, uint64_t *evals) {
+  if (!ctx || !pocket || !batch || !conformation || !out) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  Staged st;
+  vs_status rc;
+  if ((rc = stage(ctx, batch, 0, batch->n_ligands, st))) return rc;
+  if ((rc = h2d(ctx->aux0, conformation, 3 * static_cast<size_t>(st.atoms), ctx->stream))) return rc;
+  CUDA_TRY(ctx->aux1.ensure(sizeof(double) * std::max(st.n, 1)));
+  CUDA_TRY(ctx->aux2.ensure(sizeof(unsigned long long) * std::max(st.n, 1)));
+  CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(vsd::launch_geo_score(st.b, pocket->dev(), ctx->aux0.as<double>(), ctx->aux1.as<double>(),
+                                 ctx->aux2.as<unsigned long long>(), ctx->stream));
+  if (st.n) {
+    CUDA_TRY(cudaMemcpyAsync(out, ctx->aux1.p, sizeof(double) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (evals) CUDA_TRY(cudaMemcpyAsync(evals, ctx->aux2.p, sizeof(uint64_t) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return VS_OK;
+}
+
+vs_status vs_chem_score_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                              const double *conformation, double *out) {
+  if (!ctx || !pocket || !batch || !conformation || !out) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  Staged st;
+  vs_status rc;
+  if ((rc = stage(ctx, batch, 0, batch->n_ligands, st))) return rc;
+  if ((rc = h2d(ctx->aux0, conformation, 3 * static_cast<size_t>(st.atoms), ctx->stream))) return rc;
+  CUDA_TRY(ctx->aux1.ensure(sizeof(double) * std::max(st.n, 1)));
+  CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(vsd::launch_chem_score(st.b, pocket->dev(), ctx->aux0.as<double>(), ctx->aux1.as<double>(), ctx->stream));
+  if (st.n) CUDA_TRY(cudaMemcpyAsync(out, ctx->aux1.p, sizeof(double) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return VS_OK;
+}
+
+vs_status vs_flatten_batch(vs_context *ctx, const vs_ligand_batch *batch, int32_t max_sweeps, double *conformation_out,
+                           double *angles_out, int32_t *status_out) {
+  if (!ctx || !batch || !conformation_out) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  Staged st;
+  vs_status rc;
+  if ((rc = stage(ctx, batch, 0, batch->n_ligands, st))) return rc;
+  vsd::flat_out f{};
+  if ((rc = ensure_flat(ctx, st, f))) return rc;
+  CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(vsd::launch_flatten(st.b, max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
+  std::vector<int> idx(static_cast<size_t>(std::max(st.torsions, 1)));
+  std::vector<vsd::lig_meta> meta(static_cast<size_t>(std::max(st.n, 1)));
+  if (st.atoms)
+    CUDA_TRY(cudaMemcpyAsync(conformation_out, f.xyz, sizeof(double) * 3 * st.atoms, cudaMemcpyDeviceToHost, ctx->stream));
+  if (st.torsions)
+    CUDA_TRY(cudaMemcpyAsync(idx.data(), f.idx, sizeof(int) * st.torsions, cudaMemcpyDeviceToHost, ctx->stream));
+  if (st.n)
+    CUDA_TRY(cudaMemcpyAsync(meta.data(), st.b.meta, sizeof(vsd::lig_meta) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  constexpr double step = 2.0 * kPi / 36;  // angles_of, search.cpp:40
+  if (angles_out)
+    for (int t = 0; t < st.torsions; ++t) angles_out[t] = idx[static_cast<size_t>(t)] * step;
+  if (status_out)
+    for (int i = 0; i < st.n; ++i) status_out[i] = meta[static_cast<size_t>(i)].status;
+  return VS_OK;
+}
+
+vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                                const vs_scoring_config *cfg, vs_pose *poses, double *angles, double *conformation,
+                                uint64_t *evals, int32_t *status_out) {
+  if (!ctx || !pocket || !batch || !cfg || !poses || !conformation)
+    return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  vsd::search_cfg sc{};
+  vs_status rc;
+  if ((rc = upload_tables(ctx, *cfg, 1, sc))) return rc;
+  Staged st;
+  if ((rc = stage(ctx, batch, 0, batch->n_ligands, st))) return rc;
+  std::vector<double> pin(static_cast<size_t>(8) * std::max(st.n, 1));
+  for (int i = 0; i < st.n; ++i) {
+    for (int q = 0; q < 4; ++q) pin[8 * i + q] = poses[i].rotation[q];
+    for (int q = 0; q < 3; ++q) pin[8 * i + 4 + q] = poses[i].translation[q];
+    pin[8 * i + 7] = poses[i].geo_score;
+  }
+  if ((rc = h2d(ctx->aux0, pin.data(), pin.size(), ctx->stream))) return rc;
+  if ((rc = h2d(ctx->aux1, angles ? angles : pin.data(), angles ? static_cast<size_t>(st.torsions) : 1, ctx->stream)))
+    return rc;
+  if ((rc = h2d(ctx->aux2, conformation, 3 * static_cast<size_t>(st.atoms), ctx->stream))) return rc;
+  vsd::item_out o{};
+  if ((rc = ensure_items(ctx, st, 1, o))) return rc;
+  CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
+  CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(vsd::launch_local_search(st.b, pocket->dev(), sc, ctx->aux0.as<double>(), ctx->aux1.as<double>(),
+                                    ctx->aux2.as<double>(), o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax,
+                                    ctx->num_sms, ctx->stream));
+  std::vector<double> T(static_cast<size_t>(7) * std::max(st.n, 1)), geo(static_cast<size_t>(std::max(st.n, 1)));
+  std::vector<unsigned long long> ev(static_cast<size_t>(std::max(st.n, 1)));
+  std::vector<int> stat(static_cast<size_t>(std::max(st.n, 1)));
+  if (st.n) {
+    CUDA_TRY(cudaMemcpyAsync(T.data(), o.T, sizeof(double) * 7 * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(geo.data(), o.geo, sizeof(double) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ev.data(), o.evals, sizeof(unsigned long long) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(stat.data(), o.status, sizeof(int) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (angles && st.torsions)
+    CUDA_TRY(cudaMemcpyAsync(angles, o.ang, sizeof(double) * st.torsions, cudaMemcpyDeviceToHost, ctx->stream));
+  if (st.atoms)
+    CUDA_TRY(cudaMemcpyAsync(conformation, o.conf, sizeof(double) * 3 * st.atoms, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < st.n; ++i) {
+    if (stat[static_cast<size_t>(i)] == VS_LIG_OK) {
+      for (int q = 0; q < 4; ++q) poses[i].rotation[q] = T[7 * i + q];
+      for (int q = 0; q < 3; ++q) poses[i].translation[q] = T[7 * i + 4 + q];
+      poses[i].geo_score = geo[static_cast<size_t>(i)];
+    }
+    if (evals) evals[i] = ev[static_cast<size_t>(i)];
+    if (status_out) status_out[i] = stat[static_cast<size_t>(i)];
+  }
+  return VS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Kernel launch interface of the dock path (kernels.cu).  Host driver code
+// (driver.cu) fills these argument blocks and calls the launchers.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dmath.cuh"
+
+namespace vsd {
+
+// Per-ligand derived layout written by k_setup.  Offsets into the batch
+// arrays come from the caller's atom/torsion offset arrays.
+struct lig_meta {
+  int n_atoms;
+  int n_heavy;
+  int m;
+  int status;  // vs_ligand_status
+};
+
+// Device copy of one batch (vs_ligand_batch) plus derived arrays.
+struct batch_dev {
+  int n_lig;
+  const int *atom_off;     // n+1
+  const int *bond_off;     // n+1
+  const int *tors_off;     // n+1
+  const int *ditem_base;   // n (capacity m*N per ligand)
+  const double *xyz;       // 3*atoms
+  const uint8_t *elem;
+  const uint8_t *heavy;
+  const uint16_t *bond_a;
+  const uint16_t *bond_b;
+  const uint16_t *tors_bond;
+  const int *right_off;    // torsions+1
+  const uint16_t *right_atoms;
+  // derived (k_setup)
+  lig_meta *meta;          // n
+  uint32_t *atom_tmask;    // atoms: bit t <=> atom in right_set(t)
+  uint16_t *heavy_list;    // atoms capacity: local atom index of heavy h
+  uint32_t *heavy_dmask;   // atoms capacity: bit t <=> heavy h in D_t
+  uint16_t *tors_ha;       // torsions: heavy index of bond.a
+  uint16_t *tors_hb;       // torsions: heavy index of bond.b
+  int *d_count;            // torsions: |D_t ∩ heavy|
+  int *d_off;              // torsions: offset of D_t items in the ligand list
+  uint16_t *ditems;        // ditem_base[l] + ...: heavy indices of D_t items
+};
+
+struct pocket_dev {
+  grid_view g;
+  double center[3];
+  int n_protein;
+  const double *pxyz;       // 3*P
+  const uint8_t *pclass;    // P: 0 hydrophobic, 1 polar, 2 other (chem.cpp:24-29)
+  // culling cells for chem_score
+  double cmin[3];
+  double cs;                // cell size
+  int cdims[3];
+  const int *cell_start;    // ncells+1
+  const int *cell_atoms;
+};
+
+struct search_cfg {
+  int k;
+  int rescored;
+  double rmsd_threshold;
+  int max_iter;
+  double step_t, step_r, step_q, min_t;
+  int flatten_sweeps;
+  int n_levels;             // spin table levels
+  const double *spin;       // [n_levels][6][4] (x,y,z,w), glibc trig, host computed
+  const double *fibq;       // [k][4]
+};
+
+// Per-restart scratch (item = ligand * k + restart).
+struct item_out {
+  double *geo;              // items
+  double *T;                // items * 7 (q xyzw, t xyz)
+  double *ang;              // tors_off[l]*k + r*m + t
+  double *conf;             // (atom_off[l]*k + r*N + a)*3
+  unsigned long long *evals;
+  int *status;
+};
+
+struct flat_out {
+  int *idx;                 // torsions: lattice index of the flat angle
+  double *xyz;              // 3*atoms: flat conformation
+  double *centroid;         // 3*n
+};
+
+struct dock_out {
+  void *results;            // vs_dock_result[n]
+  double *best_ang;         // torsions
+  double *best_conf;        // 3*atoms
+};
+
+void set_lattice_table(const double *sc72);
+
+cudaError_t launch_setup(const batch_dev &b, int restarts, cudaStream_t s);
+cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,
+                           cudaStream_t s);
+cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
+                          const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
+                          int num_sms, cudaStream_t s, int *launches);
+cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
+                          const dock_out &d, int nmax_atoms, cudaStream_t s);
+// sub-API kernels
+cudaError_t launch_field_values(const pocket_dev &p, int64_t n, const double *xyz, double *out, cudaStream_t s);
+cudaError_t launch_geo_score(const batch_dev &b, const pocket_dev &p, const double *conf, double *out,
+                             unsigned long long *evals, cudaStream_t s);
+cudaError_t launch_chem_score(const batch_dev &b, const pocket_dev &p, const double *conf, double *out,
+                              cudaStream_t s);
+cudaError_t launch_build_pocket(const double *hxyz, int nh, double cx, double cy, double cz, double radius,
+                                double ox, double oy, double oz, double h, int d0, int d1, int d2, double *values,
+                                cudaStream_t s);
+// local_search of one supplied pose per ligand (item = ligand, k = 1).
+cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,
+                                const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,
+                                int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s);
+
+}  // namespace vsd

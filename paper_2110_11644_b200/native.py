@@ -1,0 +1,89 @@
+"""Loader for the in-tree native library ``_lib/libvsdock.so``.
+
+The product path has no fallback: if the library is missing or no sm_100
+device is visible, GPU entry points raise immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libvsdock.so")
+
+_d = C.POINTER(C.c_double)
+_u64 = C.POINTER(C.c_uint64)
+_i32 = C.POINTER(C.c_int32)
+_PD = C.POINTER(abi.PocketDesc)
+_LB = C.POINTER(abi.LigandBatchDesc)
+_CF = C.POINTER(abi.ScoringConfig)
+_DR = C.POINTER(abi.DockResult)
+_PO = C.POINTER(abi.PoseDesc)
+_vp = C.c_void_p
+
+# (name, restype, argtypes) for every entry point of include/vs_dock.h and
+# include/vs_prep.h.
+SIGNATURES = {
+    "vs_abi_version": (C.c_int, []),
+    "vs_device_count": (C.c_int, []),
+    "vs_last_error_message": (C.c_char_p, []),
+    "vs_scoring_config_default": (None, [_CF]),
+    "vs_context_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "vs_context_destroy": (C.c_int, [_vp]),
+    "vs_context_last_timing": (C.c_int, [_vp, _d, _i32]),
+    "vs_pocket_create": (C.c_int, [_vp, _PD, C.POINTER(_vp)]),
+    "vs_pocket_build": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_uint8), _d, _d, C.c_double, C.c_double,
+                                  C.POINTER(_vp)]),
+    "vs_pocket_info": (C.c_int, [_vp, _d, _d, _i32, _i32]),
+    "vs_pocket_download": (C.c_int, [_vp, _vp, _d]),
+    "vs_pocket_destroy": (C.c_int, [_vp]),
+    "vs_dock_batch": (C.c_int, [_vp, _vp, _LB, _CF, _DR, _d, _d]),
+    "vs_field_values": (C.c_int, [_vp, _vp, C.c_int64, _d, _d]),
+    "vs_geo_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d, _u64]),
+    "vs_chem_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d]),
+    "vs_flatten_batch": (C.c_int, [_vp, _LB, C.c_int32, _d, _d, _i32]),
+    "vs_local_search_batch": (C.c_int, [_vp, _vp, _LB, _CF, _PO, _d, _d, _u64, _i32]),
+    # vs_prep.h
+    "vs_prep_smiles_batch": (C.c_int, [C.c_int32, C.POINTER(C.c_char_p), C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "vs_ligand_set_view": (C.c_int, [_vp, _LB, C.POINTER(_i32)]),
+    "vs_ligand_set_error": (C.c_char_p, [_vp, C.c_int32]),
+    "vs_ligand_set_free": (None, [_vp]),
+    "vs_synth_smiles": (C.c_int64, [C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_char_p, C.c_int64]),
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def lib():
+    """The loaded libvsdock.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                              " or `make -C paper_2110_11644_b200/csrc`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return (lib().vs_last_error_message() or b"").decode()
+
+
+def check(status: int, what: str):
+    if status != abi.VS_OK:
+        msg = last_error()
+        if status == abi.VS_ERR_INVALID_ARGUMENT:
+            raise ValueError(f"{what}: {msg}")
+        raise NativeError(f"{what} failed (status {status}): {msg}")
