@@ -48,8 +48,9 @@ def available(kind: str) -> bool:
 
 
 class Oracle:
-    def __init__(self, kind: str = "port"):
+    def __init__(self, kind: str = "port", trig: int = 0):
         self.kind = kind
+        self.trig = trig
         path = PORT_LIB if kind == "port" else REF_LIB
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} not built (run `make -C oracle` / oracle/build_ref.sh)")
@@ -78,6 +79,9 @@ class Oracle:
         self._ids = fn("internal_distance_sum", C.c_double, [C.c_int, _d])
         if kind == "port":
             self._trig = fn("set_trig_mode", C.c_int, [C.c_int])
+            self._sc_cr = fn("sincos_cr", None, [C.c_double, _d, _d])
+            self._sc_gl = fn("sincos_glibc", None, [C.c_double, _d, _d])
+            self._mat = fn("materialize", C.c_int, [_LB, _d, _PO, _d, _i32])
             self._detect = fn("detect_torsions", C.c_int, [_LB, C.c_int, _u16, _u8])
         else:
             self._prep = fn("prepare", C.c_void_p, [C.c_char_p, C.c_int, C.c_int])
@@ -94,13 +98,38 @@ class Oracle:
 
     # ------------------------------------------------------------ config
     def set_trig_mode(self, mode: int):
-        """0: glibc sin/cos (reference-faithful); 1: the GPU's correctly rounded routine."""
+        """0: glibc sin/cos (reference-faithful); 1: the GPU's correctly rounded routine.
+        The mode is per Oracle object and applied before every call (the
+        library keeps one global switch)."""
         assert self.kind == "port"
-        self._trig(mode)
+        self.trig = mode
+
+    def _apply_trig(self):
+        if self.kind == "port":
+            self._trig(self.trig)
+
+    def sincos(self, x: float, correctly_rounded: bool = True):
+        s, c = C.c_double(), C.c_double()
+        (self._sc_cr if correctly_rounded else self._sc_gl)(x, C.byref(s), C.byref(c))
+        return s.value, c.value
+
+    def materialize(self, batch: LigandBatch, angles: np.ndarray, poses: np.ndarray) -> np.ndarray:
+        """apply_rigid(apply_torsions(base, angles), T) per ligand (pose.hpp:20-22)."""
+        self._apply_trig()
+        ang = np.ascontiguousarray(angles, dtype=np.float64)
+        if ang.size == 0:
+            ang = np.zeros(1)
+        poses = np.ascontiguousarray(poses, dtype=abi.POSE_DTYPE)
+        out = np.zeros((max(batch.n_atoms_total, 1), 3))
+        st = np.zeros(batch.n_ligands, dtype=np.int32)
+        self._mat(C.byref(batch.desc()), abi.ptr(ang, C.c_double), poses.ctypes.data_as(_PO),
+                  abi.ptr(out, C.c_double), abi.ptr(st, C.c_int32))
+        return out[:batch.n_atoms_total]
 
     # ------------------------------------------------------------ hot path
     def dock_batch(self, pocket: Pocket, batch: LigandBatch, cfg: abi.ScoringConfig, nthreads: int = 1,
                    want_conf: bool = True, want_counters: bool = False):
+        self._apply_trig()
         res = np.zeros(batch.n_ligands, dtype=abi.DOCK_RESULT_DTYPE)
         ang = np.zeros(max(batch.n_torsions_total, 1), dtype=np.float64)
         conf = np.zeros((max(batch.n_atoms_total, 1), 3), dtype=np.float64) if want_conf else None
@@ -141,6 +170,7 @@ class Oracle:
         return out
 
     def flatten(self, batch: LigandBatch, max_sweeps: int = 20, nthreads: int = 1):
+        self._apply_trig()
         conf = np.zeros((max(batch.n_atoms_total, 1), 3))
         ang = np.zeros(max(batch.n_torsions_total, 1))
         st = np.zeros(batch.n_ligands, dtype=np.int32)
@@ -150,6 +180,7 @@ class Oracle:
 
     def local_search(self, pocket: Pocket, batch: LigandBatch, cfg, poses: np.ndarray, angles: np.ndarray,
                      conf: np.ndarray):
+        self._apply_trig()
         poses = poses.copy()
         angles = np.ascontiguousarray(angles, dtype=np.float64).copy()
         if angles.size == 0:
@@ -163,6 +194,7 @@ class Oracle:
         return poses, angles[:batch.n_torsions_total], conf, ev, st
 
     def initial_poses(self, pocket: Pocket, batch: LigandBatch, flat_angles: np.ndarray, k: int):
+        self._apply_trig()
         lig = batch.ligands[0]
         fa = np.ascontiguousarray(flat_angles, dtype=np.float64)
         if fa.size == 0:
@@ -188,6 +220,7 @@ class Oracle:
         return order[:n]
 
     def exhaustive_dock(self, pocket: Pocket, batch: LigandBatch):
+        self._apply_trig()
         pose = np.zeros(1, dtype=abi.POSE_DTYPE)
         conf = np.zeros((batch.ligands[0].n_atoms, 3))
         rc = self._exh(C.byref(pocket.desc()), C.byref(batch.desc()), pose.ctypes.data_as(_PO),

@@ -1099,4 +1099,37 @@ int vso_detect_torsions(const vs_ligand_batch *b, int i, uint16_t *bonds_out, ui
   return m;
 }
 
+// The correctly rounded routine the GPU uses (include/vs_crtrig.h), host build.
+void vso_sincos_cr(double x, double *s, double *c) { vs_crtrig::sincos_cr(x, s, c); }
+void vso_sincos_glibc(double x, double *s, double *c) {
+  *s = std::sin(x);
+  *c = std::cos(x);
+}
+
+// Canonical pose materialisation (pose.hpp:20-22): per ligand,
+// apply_rigid(apply_torsions(base, angles), T).  poses: vs_pose per ligand.
+int vso_materialize(const vs_ligand_batch *b, const double *angles, const vs_pose *poses, double *conf_out,
+                    int32_t *status) {
+  for (int i = 0; i < b->n_ligands; ++i) {
+    try {
+      const Ligand lig = ligand_from_batch(b, i);
+      std::vector<double> a(angles + b->torsion_offset[i], angles + b->torsion_offset[i + 1]);
+      RT T;
+      T.q = {poses[i].rotation[0], poses[i].rotation[1], poses[i].rotation[2], poses[i].rotation[3]};
+      T.t = {poses[i].translation[0], poses[i].translation[1], poses[i].translation[2]};
+      const Conf c = apply_rigid(apply_torsions(lig.pos, lig, a, nullptr), T);
+      for (std::size_t k = 0; k < c.size(); ++k) {
+        const int g = b->atom_offset[i] + static_cast<int>(k);
+        conf_out[3 * g] = c[k].x;
+        conf_out[3 * g + 1] = c[k].y;
+        conf_out[3 * g + 2] = c[k].z;
+      }
+      if (status) status[i] = VS_LIG_OK;
+    } catch (const LigandError &e) {
+      if (status) status[i] = e.code;
+    }
+  }
+  return VS_OK;
+}
+
 }  // extern "C"
