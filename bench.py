@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""Benchmark: ligands docked+scored per second (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): one 3CL-sized synthetic pocket
+(build_pocket radius 12 A, spacing 0.375 A -> 65^3 nodes, 2,400 protein
+heavy atoms), synthetic drug-like ligands (~30 heavy atoms, 5-7 rotatable
+bonds, prepared with prepare_ligand and quantised to the f32 wire format),
+30 restarts, 30 rescored.  A step docks one batch of ligands per GPU
+(default 131,072; the default 8 timed steps dock 1,048,576 ligands = the 1M
+library of configs[1]).  Multi-GPU: one process per GPU, each docks its own
+shard (weak scaling, no data-path collective); the host top-K merge of
+merge.cpp:131-135 runs after the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value` is device throughput with the batch already staged in HBM (CUDA
+events around the kernels on the context stream, max over ranks); `e2e` is
+the same metric through the public API (vs_dock_batch) with pinned host
+buffers, H2D of the ligand SoA and D2H of the results inside the timed
+region.  `--impl reference` times the reference's own CPU code
+(oracle/_ref: the reference sources compiled unchanged) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ligands docked+scored/sec"
+UNIT = "ligands/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=131072, help="ligands per GPU per step")
+    p.add_argument("--restarts", type=int, default=30)
+    p.add_argument("--rescored", type=int, default=30)
+    p.add_argument("--seed", type=int, default=20260819)
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU baseline sample length")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+def pinned_like(a: np.ndarray) -> np.ndarray:
+    import torch
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    out = t.numpy().view(a.dtype).reshape(a.shape)
+    out[...] = a
+    out._keep = t  # noqa: keep the pinned storage alive
+    return out
+
+
+def pin_batch(b):
+    """Move the SoA arrays of a LigandBatch into pinned host memory."""
+    for name in ("atom_offset", "xyz", "element", "is_heavy", "bond_offset", "bond_a", "bond_b", "bond_order",
+                 "torsion_offset", "torsion_bond", "right_offset", "right_atoms"):
+        setattr(b, name, pinned_like(getattr(b, name)))
+    b._desc = None
+    return b
+
+
+def flop_model(counters: np.ndarray) -> dict:
+    """SURVEY.md §8(d)/Appendix B algorithmic FP64 work, split by stage.
+    F = 48 S + 18 A_rigid + 21 A_tors + 30 R_build + 10 P_flat + 14 P_chem + 9 P_rmsd."""
+    c = counters.astype(np.float64).sum(axis=0)
+    S, A_rigid, A_tors, R_build, P_flat, P_chem, P_rmsd = c[:7]
+    total = 48 * S + 18 * A_rigid + 21 * A_tors + 30 * R_build + 10 * P_flat + 14 * P_chem + 9 * P_rmsd
+    return {"S": S, "A_rigid": A_rigid, "A_tors": A_tors, "R_build": R_build, "P_flat": P_flat, "P_chem": P_chem,
+            "P_rmsd": P_rmsd, "F_total": total}
+
+
+def split_flops(counters: np.ndarray, batch, k: int) -> dict:
+    """Per-stage algorithmic flops (search / flatten / select) from the
+    per-ligand counters and the batch structure."""
+    c = counters.astype(np.float64)
+    N = np.diff(batch.atom_offset).astype(np.float64)
+    m = np.diff(batch.torsion_offset).astype(np.float64)
+    rall = np.array([sum(len(r) for r in lig.right_sets) for lig in batch.ligands], dtype=np.float64)
+    pairs = N * (N - 1) / 2
+    cand = np.where(pairs > 0, c[:, 4] / np.maximum(pairs, 1), 0)
+    a_tors_flat = cand * rall
+    r_flat = cand * m + m
+    flatten = 10 * c[:, 4] + 21 * a_tors_flat + 30 * r_flat
+    select = 14 * c[:, 5] + 9 * c[:, 6]
+    search = 48 * c[:, 0] + 18 * c[:, 1] + 21 * (c[:, 2] - a_tors_flat) + 30 * (c[:, 3] - r_flat)
+    return {"search": float(search.sum()), "flatten": float(flatten.sum()), "select": float(select.sum())}
+
+
+def measure_fp64_peak(device: int) -> dict:
+    from paper_2110_11644_b200 import native
+    import ctypes as C
+    L = native.lib()
+    out = (C.c_double * 3)()
+    L.vs_measure_peaks(device, out)
+    return {"fp64_dadd_ops": out[0], "fp64_fma_flops": out[1], "fp32_fma_flops": out[2]}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_dock_rate(pocket_host, ligs, cfg, seconds: float, threads: int):
+    """Time the reference's own CPU dock_and_score (oracle/_ref; the oracle
+    restatement if _ref is absent) on a bounded sample of the workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, available
+    from paper_2110_11644_b200.model import LigandBatch
+    kind = "ref" if available("ref") else "port"
+    o = Oracle(kind)
+    probe = LigandBatch(ligs[:threads])
+    t = time.perf_counter()
+    o.dock_batch(pocket_host, probe, cfg, nthreads=threads, want_conf=False)
+    dt = max(time.perf_counter() - t, 1e-3)
+    per_lig = dt / max(1, len(probe.ligands)) * threads
+    n = int(min(len(ligs), max(threads, seconds * threads / per_lig)))
+    n = max(threads, (n // threads) * threads)
+    sample = LigandBatch(ligs[:n])
+    t = time.perf_counter()
+    o.dock_batch(pocket_host, sample, cfg, nthreads=threads, want_conf=False)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "reference" if kind == "ref" else "port",
+            "sample": f"{n} ligands of the same library (k={cfg.restarts}), {dt:.1f} s on {threads} host threads"}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    from paper_2110_11644_b200 import api, synth
+    from paper_2110_11644_b200.model import LigandBatch
+
+    cfg = api.ScoringConfig(restarts=args.restarts, rescored=args.rescored)
+    threads = os.cpu_count() or 8
+    workload = (f"configs[1]: 3CL-sized synthetic pocket (65^3, 2400 protein atoms), drug-like ligands "
+                f"(~30 heavy / 5-7 rotors), k={args.restarts}, rescored={args.rescored}; "
+                f"{args.batch} ligands per GPU per step")
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        el, xyz = synth.synthetic_protein()
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Oracle, available
+        if not available("ref") and not available("port"):
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return
+        kind = "ref" if available("ref") else "port"
+        ref = Oracle("ref") if kind == "ref" else None
+        pocket_host = ref.build_pocket(el, xyz, [0, 0, 0], 12.0, 0.375) if ref else None
+        smi = api.synthetic_smiles(max(threads * 256, 4096), seed=args.seed + 1)
+        # parse/hydrogens/embed/torsions on the host (bit-identical to the
+        # reference's, tests/test_prep.py), then prepare_ligand's flatten with
+        # the reference's own code, then the f32 wire quantisation.
+        from paper_2110_11644_b200.model import LigandBatch as _LB
+        raw = api.prepare_smiles(smi, mode=1, nthreads=threads)
+        flat_o = ref if ref is not None else Oracle("port")
+        fc, _, fst = flat_o.flatten(_LB(raw), 20, nthreads=threads)
+        bb = _LB(raw)
+        ligs = [l.with_xyz(fc[bb.atom_offset[i]:bb.atom_offset[i + 1]]).quantized() for i, l in enumerate(raw)]
+        rates = []
+        for i in range(args.warmup + args.steps):
+            r = cpu_dock_rate(pocket_host, ligs, cfg, max(2.0, args.cpu_seconds / 2), threads)
+            if i >= args.warmup:
+                rates.append(r)
+        v = statistics.median([r["value"] for r in rates])
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload, "host_threads": threads},
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": rates[-1]["kind"],
+                                 "sample": rates[-1]["sample"]},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    ctx = api.default_context(local)
+    # ---- setup: pocket + ligand library (outside the timed region)
+    t_setup = time.perf_counter()
+    el, xyz = synth.synthetic_protein()
+    pocket = api.build_pocket(el, xyz, [0.0, 0.0, 0.0], 12.0, 0.375, ctx)
+    smi = api.synthetic_smiles(args.batch, seed=args.seed + 1 + 7919 * rank)
+    ligs = api.prepare_ligand(smi, quantize=True, ctx=ctx, nthreads=threads)
+    batch = pin_batch(LigandBatch(ligs))
+    from paper_2110_11644_b200 import abi
+    res_buf = pinned_like(np.zeros(batch.n_ligands, dtype=abi.DOCK_RESULT_DTYPE))
+    ang_buf = pinned_like(np.zeros(max(batch.n_torsions_total, 1)))
+    out = {"results": res_buf, "angles": ang_buf}
+    setup_s = time.perf_counter() - t_setup
+    h2d = sum(getattr(batch, n).nbytes for n in ("atom_offset", "xyz", "element", "is_heavy", "bond_offset", "bond_a",
+                                                  "bond_b", "bond_order", "torsion_offset", "torsion_bond",
+                                                  "right_offset", "right_atoms"))
+    d2h = res_buf.nbytes + 8 * batch.n_torsions_total
+
+    import torch
+    torch.cuda.set_device(local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def step(counters=False):
+        return api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False, out=out,
+                                        want_counters=counters)
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        step()
+    clocks = ClockSampler(local)
+    dev_ms, wall_s, stages, launches = [], [], [], 0
+    last = None
+    clocks.start()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # evict L2 between timed steps (256 MB > 126 MB L2)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        last = step(counters=(i == args.steps - 1))
+        torch.cuda.synchronize()
+        wall_s.append(time.perf_counter() - t0)
+        dev_ms.append(last.kernel_ms)
+        stages.append(last.stage_ms)
+        launches += last.launches
+    clk = clocks.stop()
+    tot_dev = sum(dev_ms) / 1e3
+    tot_wall = sum(wall_s)
+    if dist is not None:
+        t = torch.tensor([tot_dev, tot_wall], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_dev, tot_wall = float(t[0]), float(t[1])
+    ligands_total = world * args.steps * batch.n_ligands
+    value = ligands_total / tot_dev
+    e2e = ligands_total / tot_wall
+    status = last.results["status"]
+    ok = int((status == 0).sum())
+
+    # host top-K merge (merge.cpp:131-135: score desc, SMILES asc) of the last step
+    K = 1000
+    order = np.lexsort((np.array(smi), -last.results["best_score"]))[:K]
+    top_local = [(float(last.results["best_score"][i]), smi[i]) for i in order]
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, top_local)
+        merged = sorted([x for g in gathered for x in g], key=lambda x: (-x[0], x[1]))[:K]
+    else:
+        merged = top_local
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (k_search) from the algorithmic FP64 work
+    fl = split_flops(last.counters, batch, args.restarts)
+    st_last = last.stage_ms
+    peaks = measure_fp64_peak(local)
+    search_s = st_last["search"] / 1e3
+    achieved = fl["search"] / search_s / 1e12
+    peak = peaks["fp64_dadd_ops"] / 1e12
+    total_f = fl["search"] + fl["flatten"] + fl["select"]
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_dock_rate(pocket.to_host(), ligs, cfg, args.cpu_seconds, threads)
+        except Exception as e:  # pragma: no cover - reported, not hidden
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "unavailable", "sample": repr(e)}
+    stage_mean = {k: float(np.mean([s[k] for s in stages])) for k in stages[0]}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_dev / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "ligands_per_step": world * batch.n_ligands,
+                   "pocket": "build_pocket(r=12 A, h=0.375 A) -> 65^3, synthetic protein seed 20260819",
+                   "l2": "flushed between timed steps (256 MB device write)", "parallelism": f"replica x{world}",
+                   "setup_s": round(setup_s, 2)},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_search (initial_poses + local_search)",
+                     "flops_per_launch": fl["search"], "launch_ms": st_last["search"],
+                     "peak_source": "measured live: FP64 DADD/DMUL issue rate (no FMA: -fmad=false)",
+                     "whole_step_frac": total_f / (sum(st_last.values()) / 1e3) / 1e12 / peak,
+                     "fp32_fma_peak_tflops": peaks["fp32_fma_flops"] / 1e12,
+                     "fp64_fma_peak_tflops": peaks["fp64_fma_flops"] / 1e12},
+        "stage_ms_per_step": stage_mean,
+        "clocks": clk,
+        "results": {"ok": ok, "ligands": int(batch.n_ligands), "mean_best_score": float(np.mean(last.results["best_score"])),
+                    "evals_per_ligand": float(np.mean(last.results["scoring_evals"])),
+                    "topk_merged": len(merged), "top1": merged[0] if merged else None},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

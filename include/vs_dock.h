@@ -158,6 +158,9 @@ vs_status vs_context_destroy(vs_context *ctx);
  * (CUDA events around its kernels on the context stream) and the number of
  * kernel launches it issued. */
 vs_status vs_context_last_timing(vs_context *ctx, double *kernel_ms, int32_t *launches);
+/* Per-stage device milliseconds of the last vs_dock_batch: setup, flatten,
+ * search (initial_poses + local_search), select (cluster + chem + best). */
+vs_status vs_context_stage_timing(vs_context *ctx, double stage_ms[4]);
 
 /* ---- pocket: uploaded once, device resident -------- */
 vs_status vs_pocket_create(vs_context *ctx, const vs_pocket_desc *desc, vs_pocket **out);
@@ -178,6 +181,14 @@ vs_status vs_pocket_destroy(vs_pocket *p);
 vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
                         const vs_scoring_config *cfg, vs_dock_result *results,
                         double *best_angles, double *best_conformation);
+
+/* vs_dock_batch plus, when counters != NULL, the SURVEY.md Appendix B work
+ * counters per ligand (9 each: S, A_rigid, A_tors, R_build, P_flat, P_chem,
+ * P_rmsd, clash_pairs, oob_samples), reproduced from the run's integers in
+ * the oracle's (reference-order) accounting. */
+vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                           const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
+                           double *best_conformation, uint64_t *counters);
 
 /* ---- sub-APIs beneath dock_and_score (same kernels, exposed for parity) -- */
 /* pocket_field_value (grid.cpp:59-91) at n points (3*n doubles). */
@@ -202,6 +213,11 @@ vs_status vs_flatten_batch(vs_context *ctx, const vs_ligand_batch *batch, int32_
 vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
                                 const vs_scoring_config *cfg, vs_pose *poses, double *angles,
                                 double *conformation, uint64_t *evals, int32_t *status_out);
+
+/* ---- measurement helper ------------------------------------------------- */
+/* Measured FP64 DADD ops/s, FP64 DFMA flop/s and FP32 FFMA flop/s of the
+ * device (the roofline denominators of this CUDA-core path). */
+int vs_measure_peaks(int device, double out[3]);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,11 @@ class Context:
         native.lib().vs_context_last_timing(self.handle, C.byref(ms), C.byref(launches))
         return ms.value, launches.value
 
+    def stage_timing(self) -> dict:
+        ms = np.zeros(4)
+        native.lib().vs_context_stage_timing(self.handle, abi.ptr(ms, C.c_double))
+        return dict(zip(("setup", "flatten", "search", "select"), ms.tolist()))
+
     def close(self):
         if self.handle:
             native.lib().vs_context_destroy(self.handle)
@@ -315,6 +320,8 @@ class BatchResult:
     batch: LigandBatch
     kernel_ms: float = 0.0
     launches: int = 0
+    counters: np.ndarray | None = None   # (n, 9) Appendix B counters when requested
+    stage_ms: dict | None = None
 
     def result(self, i: int) -> DockResult:
         r = self.results[i]
@@ -332,7 +339,8 @@ class BatchResult:
 
 
 def dock_and_score_batch(pocket, ligands, config: ScoringConfig | None = None, ctx: Context | None = None,
-                         want_conformation: bool = True, out: dict | None = None) -> BatchResult:
+                         want_conformation: bool = True, out: dict | None = None,
+                         want_counters: bool = False) -> BatchResult:
     """dock_and_score over a batch (search.cpp:238-276).  `out` may supply
     preallocated (e.g. pinned) result arrays: keys results/angles/conf."""
     ctx = ctx or default_context()
@@ -349,12 +357,15 @@ def dock_and_score_batch(pocket, ligands, config: ScoringConfig | None = None, c
     conf = out.get("conf") if want_conformation else None
     if conf is None and want_conformation:
         conf = np.zeros((max(b.n_atoms_total, 1), 3))
-    native.check(native.lib().vs_dock_batch(ctx.handle, dp.handle, C.byref(b.desc()), C.byref(cfg),
-                                            res.ctypes.data_as(C.POINTER(abi.DockResult)), abi.ptr(ang, C.c_double),
-                                            abi.ptr(conf, C.c_double)), "vs_dock_batch")
+    counters = np.zeros((max(b.n_ligands, 1), 9), dtype=np.uint64) if want_counters else None
+    native.check(native.lib().vs_dock_batch_ex(ctx.handle, dp.handle, C.byref(b.desc()), C.byref(cfg),
+                                               res.ctypes.data_as(C.POINTER(abi.DockResult)),
+                                               abi.ptr(ang, C.c_double), abi.ptr(conf, C.c_double),
+                                               abi.ptr(counters, C.c_uint64)), "vs_dock_batch")
     ms, launches = ctx.last_timing()
     return BatchResult(res[:b.n_ligands], ang[:b.n_torsions_total],
-                       conf[:b.n_atoms_total] if conf is not None else None, b, ms, launches)
+                       conf[:b.n_atoms_total] if conf is not None else None, b, ms, launches,
+                       counters[:b.n_ligands] if counters is not None else None, ctx.stage_timing())
 
 
 def dock_and_score(pocket, ligand: Ligand, config: ScoringConfig | None = None,

@@ -68,6 +68,8 @@ struct vs_context {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evs[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double stage_ms[4] = {0, 0, 0, 0};  // setup, flatten, search, select
   double last_ms = 0.0;
   int last_launches = 0;
   std::mutex mu;
@@ -76,8 +78,9 @@ struct vs_context {
   // derived
   DevBuf meta, tmask, heavy_list, dmask, tors_ha, tors_hb, d_count, d_off, ditems;
   // flatten / search / select
-  DevBuf flat_idx, flat_xyz, flat_centroid, out_geo, out_T, out_ang, out_conf, out_evals, out_status, work;
-  DevBuf results, best_ang, best_conf, spin, fibq;
+  DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
+      out_iters, out_adopts, work;
+  DevBuf results, best_ang, best_conf, counters, spin, fibq;
   DevBuf aux0, aux1, aux2, aux3;
 };
 
@@ -421,6 +424,8 @@ vs_status ensure_items(vs_context *ctx, const Staged &st, int k, vsd::item_out &
   CUDA_TRY(ctx->out_conf.ensure(sizeof(double) * 3 * std::max<size_t>(1, static_cast<size_t>(st.atoms) * k)));
   CUDA_TRY(ctx->out_evals.ensure(sizeof(unsigned long long) * items));
   CUDA_TRY(ctx->out_status.ensure(sizeof(int) * items));
+  CUDA_TRY(ctx->out_iters.ensure(sizeof(int) * items));
+  CUDA_TRY(ctx->out_adopts.ensure(sizeof(int) * items));
   CUDA_TRY(ctx->work.ensure(sizeof(int) * 4));
   o.geo = ctx->out_geo.as<double>();
   o.T = ctx->out_T.as<double>();
@@ -428,6 +433,8 @@ vs_status ensure_items(vs_context *ctx, const Staged &st, int k, vsd::item_out &
   o.conf = ctx->out_conf.as<double>();
   o.evals = ctx->out_evals.as<unsigned long long>();
   o.status = ctx->out_status.as<int>();
+  o.iters = ctx->out_iters.as<int>();
+  o.adopts = ctx->out_adopts.as<int>();
   return VS_OK;
 }
 
@@ -435,6 +442,8 @@ vs_status ensure_flat(vs_context *ctx, const Staged &st, vsd::flat_out &f) {
   CUDA_TRY(ctx->flat_idx.ensure(sizeof(int) * std::max(st.torsions, 1)));
   CUDA_TRY(ctx->flat_xyz.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
   CUDA_TRY(ctx->flat_centroid.ensure(sizeof(double) * 3 * std::max(st.n, 1)));
+  CUDA_TRY(ctx->flat_sweeps.ensure(sizeof(int) * std::max(st.n, 1)));
+  f.sweeps = ctx->flat_sweeps.as<int>();
   f.idx = ctx->flat_idx.as<int>();
   f.xyz = ctx->flat_xyz.as<double>();
   f.centroid = ctx->flat_centroid.as<double>();
@@ -494,6 +503,7 @@ vs_status vs_context_create(int device, vs_context **out) {
   }
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
+  for (auto &e : ctx->evs) cudaEventCreate(&e);
   ensure_lattice(device);
   *out = ctx;
   return VS_OK;
@@ -505,6 +515,7 @@ vs_status vs_context_destroy(vs_context *ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
+  for (auto &e : ctx->evs) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return VS_OK;
@@ -514,6 +525,12 @@ vs_status vs_context_last_timing(vs_context *ctx, double *kernel_ms, int32_t *la
   if (!ctx) return fail(VS_ERR_INVALID_ARGUMENT, "null context");
   if (kernel_ms) *kernel_ms = ctx->last_ms;
   if (launches) *launches = ctx->last_launches;
+  return VS_OK;
+}
+
+vs_status vs_context_stage_timing(vs_context *ctx, double stage_ms[4]) {
+  if (!ctx || !stage_ms) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  for (int i = 0; i < 4; ++i) stage_ms[i] = ctx->stage_ms[i];
   return VS_OK;
 }
 
@@ -616,6 +633,12 @@ vs_status vs_pocket_destroy(vs_pocket *p) {
 vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
                         const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
                         double *best_conformation) {
+  return vs_dock_batch_ex(ctx, pocket, batch, cfg, results, best_angles, best_conformation, nullptr);
+}
+
+vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                           const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
+                           double *best_conformation, uint64_t *counters) {
   if (!ctx || !pocket || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
   vs_status rc = check_cfg(cfg);
   if (rc) return rc;
@@ -626,8 +649,9 @@ vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligan
   if ((rc = upload_tables(ctx, *cfg, k, sc))) return rc;
   const vsd::pocket_dev pd = pocket->dev();
   ctx->last_launches = 0;
+  for (double &x : ctx->stage_ms) x = 0.0;
   float total_ms = 0.0f;
-  const std::vector<int> cut = chunks(batch, k, size_t(3) << 30);
+  const std::vector<int> cut = chunks(batch, k, size_t(12) << 30);
   for (size_t ci = 0; ci + 1 < cut.size(); ++ci) {
     const int l0 = cut[ci], l1 = cut[ci + 1];
     Staged st;
@@ -639,15 +663,20 @@ vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligan
     CUDA_TRY(ctx->results.ensure(sizeof(vs_dock_result) * std::max(st.n, 1)));
     CUDA_TRY(ctx->best_ang.ensure(sizeof(double) * std::max(st.torsions, 1)));
     CUDA_TRY(ctx->best_conf.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
-    vsd::dock_out d{ctx->results.p, ctx->best_ang.as<double>(), ctx->best_conf.as<double>()};
+    CUDA_TRY(ctx->counters.ensure(sizeof(uint64_t) * 9 * std::max(st.n, 1)));
+    vsd::dock_out d{ctx->results.p, ctx->best_ang.as<double>(), ctx->best_conf.as<double>(),
+                    counters ? ctx->counters.as<unsigned long long>() : nullptr, f.sweeps};
     CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
-    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->evs[0], ctx->stream));
     CUDA_TRY(vsd::launch_setup(st.b, k, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->evs[1], ctx->stream));
     CUDA_TRY(vsd::launch_flatten(st.b, cfg->flatten_max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
     CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax, ctx->num_sms,
                                 ctx->stream, nullptr));
+    CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
     CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
-    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));
     ctx->last_launches += 4;
     CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,
                              ctx->stream));
@@ -658,9 +687,17 @@ vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligan
     if (best_conformation && st.atoms)
       CUDA_TRY(cudaMemcpyAsync(best_conformation + 3 * static_cast<size_t>(A0), ctx->best_conf.p,
                                sizeof(double) * 3 * st.atoms, cudaMemcpyDeviceToHost, ctx->stream));
+    if (counters)
+      CUDA_TRY(cudaMemcpyAsync(counters + 9 * static_cast<size_t>(l0), ctx->counters.p, sizeof(uint64_t) * 9 * st.n,
+                               cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ctx->evs[i], ctx->evs[i + 1]);
+      ctx->stage_ms[i] += ms;
+    }
     float ms = 0.0f;
-    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    cudaEventElapsedTime(&ms, ctx->evs[0], ctx->evs[4]);
     total_ms += ms;
   }
   ctx->last_ms = total_ms;

@@ -45,7 +45,7 @@ __global__ void k_setup(batch_dev b, int restarts) {
   const int a0 = b.atom_off[l], N = b.atom_off[l + 1] - a0;
   const int b0 = b.bond_off[l], nb = b.bond_off[l + 1] - b0;
   const int t0 = b.tors_off[l], m = b.tors_off[l + 1] - t0;
-  lig_meta meta{N, 0, m, VS_LIG_OK};
+  lig_meta meta{N, 0, m, VS_LIG_OK, 0, 0};
   // apply_torsion's index checks (transform.cpp:56-57, 66-67) fire in the
   // first flatten pass, before any coordinate is used.
   if (m > VS_MAX_TORSIONS) meta.status = VS_LIG_TOO_LARGE;
@@ -83,7 +83,11 @@ __global__ void k_setup(batch_dev b, int restarts) {
   }
   for (int h = 0; h < n; ++h) b.heavy_dmask[a0 + h] = 0u;
   for (int t = 0; t < m; ++t)
-    for (int r = b.right_off[t0 + t]; r < b.right_off[t0 + t + 1]; ++r) b.atom_tmask[a0 + b.right_atoms[r]] |= 1u << t;
+    for (int r = b.right_off[t0 + t]; r < b.right_off[t0 + t + 1]; ++r) {
+      b.atom_tmask[a0 + b.right_atoms[r]] |= 1u << t;
+      meta.r_all += 1;
+      meta.r_heavy += b.heavy[a0 + b.right_atoms[r]] ? 1 : 0;
+    }
   // Heavy index of each torsion endpoint (the search tracks heavy atoms).
   for (int t = 0; t < m; ++t) {
     const int bi = b.tors_bond[t0 + t];
@@ -161,14 +165,18 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
   double *spread = cand + 3 * N * CB;  // 36
   double *mat = spread + 36;       // 12 (prefix advance)
   __shared__ int idx[VS_MAX_TORSIONS + 1];
-  __shared__ int changed, bad;
+  __shared__ int changed, bad, sweeps_done;
   const double *base = b.xyz + 3 * (size_t)a0;
   const uint32_t *tm = b.atom_tmask + a0;
   const int b0 = b.bond_off[l];
   if (tid < m) idx[tid] = 0;
-  if (tid == 0) bad = 0;
+  if (tid == 0) {
+    bad = 0;
+    sweeps_done = 0;
+  }
   __syncthreads();
   for (int sweep = 0; sweep < max_sweeps && m > 0; ++sweep) {
+    if (tid == 0) sweeps_done = sweep + 1;
     for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
     if (tid == 0) changed = 0;
     __syncthreads();
@@ -259,12 +267,31 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
     if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
     return;
   }
-  if (m == 0)
-    for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
+  // flat conformation = apply_torsions(base, angles_of(index)) (search.cpp:67-68)
+  for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
   __syncthreads();
+  for (int t = 0; t < m; ++t) {
+    if (tid == 0) {
+      const int bi = b.tors_bond[t0 + t];
+      const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+      double s, c;
+      lattice_sc(idx[t], s, c);
+      if (!torsion_setup(ld3(P + 3 * ea), ld3(P + 3 * eb), s, c, mat)) bad = 1;
+    }
+    __syncthreads();
+    if (bad) break;
+    for (int a = tid; a < N; a += blockDim.x)
+      if ((tm[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(mat, ld3(P + 3 * a)));
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
+    return;
+  }
   for (int i = tid; i < 3 * N; i += blockDim.x) f.xyz[3 * (size_t)a0 + i] = P[i];
   if (tid < m) f.idx[t0 + tid] = idx[tid];
   if (tid < 3) f.centroid[3 * l + tid] = centroid_row(P, N, tid);
+  if (tid == 0) f.sweeps[l] = sweeps_done;
 }
 
 cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,
@@ -495,7 +522,7 @@ __global__ void __launch_bounds__(128) k_search(search_args A) {
     __syncwarp();
 
     // ---- local_search (search.cpp:121-191)
-    int level = 0;
+    int level = 0, n_iter = 0, n_adopt = 0;
     bool failed = false;
     for (int iter = 0; iter < A.c.max_iter && S[S_STEPT] >= A.c.min_t; ++iter) {
       if (lane < 3) S[S_PIV + lane] = centroid_row(conf, N, lane);
@@ -608,6 +635,8 @@ __global__ void __launch_bounds__(128) k_search(search_args A) {
         }
       }
       const bool improved = bv > S[S_GEO];
+      ++n_iter;
+      n_adopt += improved ? 1 : 0;
       __syncwarp();
       if (improved) {
         if (bj < 12) {
@@ -665,6 +694,8 @@ __global__ void __launch_bounds__(128) k_search(search_args A) {
       A.o.geo[item] = S[S_GEO];
       A.o.evals[item] = evals;
       A.o.status[item] = VS_LIG_OK;
+      if (A.o.iters) A.o.iters[item] = n_iter;
+      if (A.o.adopts) A.o.adopts[item] = n_adopt;
     }
     __syncwarp();
   }
@@ -763,7 +794,8 @@ __device__ __forceinline__ double chem_weight(int a, int b) {
 }
 __device__ __forceinline__ int chem_class_of(uint8_t e) { return e == 0 ? 0 : ((e == 1 || e == 2) ? 1 : 2); }
 
-__device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, double &total, int &clashes) {
+__device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, double &total, int &clashes,
+                                          int &pairs) {
   int lo = 0, hi = p.n_protein;
   const int *list = nullptr;
   const int cx = (int)floor((x.x - p.cmin[0]) / p.cs);
@@ -780,6 +812,7 @@ __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, dou
     const d3 pp{__ldg(p.pxyz + 3 * j), __ldg(p.pxyz + 3 * j + 1), __ldg(p.pxyz + 3 * j + 2)};
     const double d = sqrt(sqn3(sub3(x, pp)));
     if (d >= 4.5) continue;
+    ++pairs;
     const double ramp = d <= 3.5 ? 1.0 : (4.5 - d) / (4.5 - 3.5);
     total += chem_weight(ci, p.pclass[j]) * ramp;
     if (d < 2.0) {
@@ -790,15 +823,18 @@ __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, dou
 }
 
 __device__ double chem_pose(const pocket_dev &p, const double *conf, const uint16_t *hl, const uint8_t *elem, int n,
-                            int &clashes) {
+                            int &clashes, int &pairs) {
   double total = 0.0;
   clashes = 0;
+  pairs = 0;
   for (int h = 0; h < n; ++h) {
     const int a = hl[h];
-    chem_atom(p, ld3(conf + 3 * a), chem_class_of(elem[a]), total, clashes);
+    chem_atom(p, ld3(conf + 3 * a), chem_class_of(elem[a]), total, clashes, pairs);
   }
   return total;
 }
+
+__device__ __forceinline__ int f_sweeps_of(const dock_out &d, int l) { return d.sweeps ? d.sweeps[l] : 0; }
 
 // ============================================================== k_select
 // cluster_and_select + chem_score + best (search.cpp:195-275).  One CTA per
@@ -814,13 +850,16 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   int *followers = leaders + k;
   double *chem = reinterpret_cast<double *>(followers + k + (k & 1) + 2);  // rescored
   int *clash = reinterpret_cast<int *>(chem + k);
-  __shared__ int n_lead, n_follow, status, joined_any;
+  int *pairs = clash + k;
+  __shared__ int n_lead, n_follow, status, first_match;
+  __shared__ unsigned long long rmsd_terms;
   vs_dock_result *res = reinterpret_cast<vs_dock_result *>(d.results) + l;
   lig_meta meta = b.meta[l];
   if (tid == 0) {
     status = meta.status;
     n_lead = 0;
     n_follow = 0;
+    rmsd_terms = 0ull;
   }
   __syncthreads();
   if (status == VS_LIG_OK)
@@ -854,7 +893,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   // greedy leader clustering (search.cpp:208-223)
   for (int vi = 0; vi < k; ++vi) {
     const int idx = order[vi];
-    if (tid == 0) joined_any = 0;
+    if (tid == 0) first_match = 0x7fffffff;
     __syncthreads();
     const int nl = n_lead;
     const double *ci = confs + 3 * (size_t)idx * N;
@@ -865,11 +904,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
         const int a = hl[h];
         sum += sqn3(sub3(ld3(ci + 3 * a), ld3(cl + 3 * a)));
       }
-      if (sqrt(sum / (double)n) <= c.rmsd_threshold) joined_any = 1;
+      if (sqrt(sum / (double)n) <= c.rmsd_threshold) atomicMin(&first_match, li);
     }
     __syncthreads();
     if (tid == 0) {
-      if (joined_any)
+      // the reference stops at the first leader within threshold
+      rmsd_terms += (unsigned long long)n * (first_match != 0x7fffffff ? first_match + 1 : nl);
+      if (first_match != 0x7fffffff)
         followers[n_follow++] = idx;
       else
         leaders[n_lead++] = idx;
@@ -880,9 +921,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   // survivors: leaders then followers, truncated (search.cpp:225-235)
   for (int s = tid; s < top; s += blockDim.x) {
     const int idx = s < n_lead ? leaders[s] : followers[s - n_lead];
-    int cl = 0;
-    chem[s] = chem_pose(p, confs + 3 * (size_t)idx * N, hl, b.elem + a0, n, cl);
+    int cl = 0, pr = 0;
+    chem[s] = chem_pose(p, confs + 3 * (size_t)idx * N, hl, b.elem + a0, n, cl, pr);
     clash[s] = cl;
+    pairs[s] = pr;
   }
   __syncthreads();
   __shared__ int best_s;
@@ -930,6 +972,27 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
     rr.clash_pairs = clash[bs];
     rr.oob_samples = oob;
     *res = rr;
+    if (d.counters) {
+      // Appendix B counter model, reproduced from the run's integers.
+      unsigned long long iters = 0, adopts = 0, pchem = 0;
+      for (int r = 0; r < k; ++r) {
+        iters += (unsigned long long)o.iters[(size_t)l * k + r];
+        adopts += (unsigned long long)o.adopts[(size_t)l * k + r];
+      }
+      for (int s = 0; s < top; ++s) pchem += (unsigned long long)pairs[s];
+      const unsigned long long NN = N, nn = n, mm = m, kk = k, J = 12 + 2 * mm;
+      const unsigned long long cand = 36ull * mm * (unsigned long long)f_sweeps_of(d, l);
+      unsigned long long *cn = d.counters + 9 * (size_t)l;
+      cn[0] = ev;
+      cn[1] = kk * NN + iters * J * nn + adopts * NN;
+      cn[2] = cand * (unsigned long long)meta.r_all + iters * 2ull * mm * (unsigned long long)meta.r_heavy;
+      cn[3] = cand * mm + 2ull * mm + kk * mm + iters * 2ull * mm * mm;
+      cn[4] = cand * (NN * (NN - 1) / 2);
+      cn[5] = pchem;
+      cn[6] = rmsd_terms;
+      cn[7] = (unsigned long long)clash[bs];
+      cn[8] = (unsigned long long)oob;
+    }
   }
 }
 
@@ -938,7 +1001,7 @@ cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_
   (void)nmax_atoms;
   if (b.n_lig == 0) return cudaSuccess;
   const int k = c.k;
-  const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + sizeof(int) * k + 16;
+  const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + 2 * sizeof(int) * k + 16;
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d);
   return cudaGetLastError();
@@ -993,8 +1056,8 @@ __global__ void k_chem(batch_dev b, pocket_dev p, const double *conf, double *ou
   const lig_meta meta = b.meta[l];
   const int a0 = b.atom_off[l];
   const int n = meta.status == VS_LIG_OK || meta.status == VS_LIG_NO_HEAVY ? meta.n_heavy : 0;
-  int cl = 0;
-  out[l] = chem_pose(p, conf + 3 * (size_t)a0, b.heavy_list + a0, b.elem + a0, n, cl);
+  int cl = 0, pr = 0;
+  out[l] = chem_pose(p, conf + 3 * (size_t)a0, b.heavy_list + a0, b.elem + a0, n, cl, pr);
 }
 cudaError_t launch_chem_score(const batch_dev &b, const pocket_dev &p, const double *conf, double *out,
                               cudaStream_t s) {

@@ -15,7 +15,9 @@ struct lig_meta {
   int n_atoms;
   int n_heavy;
   int m;
-  int status;  // vs_ligand_status
+  int status;   // vs_ligand_status
+  int r_all;    // sum_t |right_set(t)|          (counter model, Appendix B)
+  int r_heavy;  // sum_t |right_set(t) ∩ heavy|
 };
 
 // Device copy of one batch (vs_ligand_batch) plus derived arrays.
@@ -79,18 +81,23 @@ struct item_out {
   double *conf;             // (atom_off[l]*k + r*N + a)*3
   unsigned long long *evals;
   int *status;
+  int *iters;               // items: local_search iterations
+  int *adopts;              // items: adopted neighbours
 };
 
 struct flat_out {
   int *idx;                 // torsions: lattice index of the flat angle
   double *xyz;              // 3*atoms: flat conformation
   double *centroid;         // 3*n
+  int *sweeps;              // n: flatten sweeps executed
 };
 
 struct dock_out {
   void *results;            // vs_dock_result[n]
   double *best_ang;         // torsions
   double *best_conf;        // 3*atoms
+  unsigned long long *counters;  // n*9 (may be NULL): S, A_rigid, A_tors, R_build, P_flat, P_chem, P_rmsd, clash, oob
+  const int *sweeps;        // flatten sweeps per ligand (flat_out.sweeps)
 };
 
 void set_lattice_table(const double *sc72);

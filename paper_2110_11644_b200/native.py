@@ -40,11 +40,14 @@ SIGNATURES = {
     "vs_pocket_download": (C.c_int, [_vp, _vp, _d]),
     "vs_pocket_destroy": (C.c_int, [_vp]),
     "vs_dock_batch": (C.c_int, [_vp, _vp, _LB, _CF, _DR, _d, _d]),
+    "vs_dock_batch_ex": (C.c_int, [_vp, _vp, _LB, _CF, _DR, _d, _d, _u64]),
+    "vs_context_stage_timing": (C.c_int, [_vp, _d]),
     "vs_field_values": (C.c_int, [_vp, _vp, C.c_int64, _d, _d]),
     "vs_geo_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d, _u64]),
     "vs_chem_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d]),
     "vs_flatten_batch": (C.c_int, [_vp, _LB, C.c_int32, _d, _d, _i32]),
     "vs_local_search_batch": (C.c_int, [_vp, _vp, _LB, _CF, _PO, _d, _d, _u64, _i32]),
+    "vs_measure_peaks": (C.c_int, [C.c_int, _d]),
     # vs_prep.h
     "vs_prep_smiles_batch": (C.c_int, [C.c_int32, C.POINTER(C.c_char_p), C.c_int32, C.c_int32, C.POINTER(_vp)]),
     "vs_ligand_set_view": (C.c_int, [_vp, _LB, C.POINTER(_i32)]),
