@@ -109,12 +109,15 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+_PINNED = []  # keeps the pinned torch storages alive
+
+
 def pinned_like(a: np.ndarray) -> np.ndarray:
     import torch
-    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
-    out = t.numpy().view(a.dtype).reshape(a.shape)
+    t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    _PINNED.append(t)
+    out = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
     out[...] = a
-    out._keep = t  # noqa: keep the pinned storage alive
     return out
 
 

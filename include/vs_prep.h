@@ -10,7 +10,9 @@
  *           (hydrogens.cpp:33-72) + embed_3d (embed.cpp:82-419) +
  *           detect_torsions (ligand.cpp:126-139) -- coordinates unflattened;
  *   mode 2: detect_torsions(parse_smiles(s)) -- heavy-atom graph, zero
- *           coordinates (no hydrogens).
+ *           coordinates (no hydrogens);
+ *   mode 3: mode 2 plus embed_3d of the heavy-atom graph (the fixtures of
+ *           the reference's tests, e.g. test_dockengine.cpp:301-313).
  *
  * Plus the seeded synthetic drug-like SMILES generator used by the bench
  * (~30 heavy atoms, ~6 rotatable bonds, reference

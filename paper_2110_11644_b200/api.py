@@ -194,6 +194,11 @@ def parse_smiles(smiles: str) -> Ligand:
     return prepare_smiles([smiles], mode=2)[0]
 
 
+def embed_heavy(smiles: str) -> Ligand:
+    """detect_torsions(parse_smiles(s)) with embed_3d coordinates, no hydrogens."""
+    return prepare_smiles([smiles], mode=3)[0]
+
+
 def embed_ligand(smiles: str) -> Ligand:
     """Hydrogens + embedding + torsions, no flatten (test_dockengine.cpp:29-33)."""
     return prepare_smiles([smiles], mode=1)[0]

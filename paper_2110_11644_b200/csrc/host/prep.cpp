@@ -624,6 +624,11 @@ Mol prepare(const std::string &smiles, int mode) {
     detect_torsions(m);
     return m;
   }
+  if (mode == 3) {  // embed_3d of the heavy-atom graph (the reference tests' fixtures)
+    m.pos = Embedder(m).run();
+    detect_torsions(m);
+    return m;
+  }
   add_hydrogens(m);
   if (!connected(m)) throw PrepError("cannot embed a disconnected graph");
   m.pos = Embedder(m).run();
@@ -666,7 +671,7 @@ extern "C" {
 
 vs_status vs_prep_smiles_batch(int32_t n, const char *const *smiles, int32_t mode, int32_t nthreads,
                                vs_ligand_set **out) {
-  if (n < 0 || !out || (mode != 1 && mode != 2)) return VS_ERR_INVALID_ARGUMENT;
+  if (n < 0 || !out || mode < 1 || mode > 3) return VS_ERR_INVALID_ARGUMENT;
   std::vector<vsprep::Mol> mols(static_cast<std::size_t>(n));
   auto *set = new vs_ligand_set;
   set->status.assign(static_cast<std::size_t>(n), 0);
