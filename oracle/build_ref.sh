@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # Compile the reference's hot-path + input-side sources UNCHANGED, where they
 # lie under /root/reference, against the Eigen-subset restatement
-# (oracle/eigen_subset) into oracle/_ref/libvsref.so.  Nothing from the
+# (third_party/eigen_subset) into oracle/_ref/libvsref.so.  Nothing from the
 # reference is copied into this repository; the output is git-ignored.
 # The reference's own build (CMake + Eigen3 + vendored doctest/CLI11) is not
 # used: it cannot run here (no Eigen, no vendor/ tree, no network).
@@ -16,7 +16,7 @@ mkdir -p "$HERE/_ref/obj"
 SRCS="dockengine/chem dockengine/grid dockengine/search dockengine/pocket_io
       geometry/transform geometry/embed geometry/hydrogens
       molmodel/ligand molmodel/binary_codec molmodel/smiles"
-FLAGS=(-std=c++20 -O3 -fPIC -w -I"$HERE/eigen_subset" -I"$REF/include" -I"$HERE/../include")
+FLAGS=(-std=c++20 -O3 -fPIC -w -I"$HERE/../third_party/eigen_subset" -I"$REF/include" -I"$HERE/../include")
 pids=()
 for s in $SRCS; do
   o="$HERE/_ref/obj/$(echo "$s" | tr / _).o"

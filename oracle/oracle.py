@@ -7,7 +7,7 @@ Python loader for the two CPU oracles:
   and a switch for the torsion trig (glibc vs the GPU's correctly rounded
   routine).
 * ``kind="ref"``: oracle/_ref/libvsref.so, the reference's OWN sources
-  compiled against oracle/eigen_subset (oracle/build_ref.sh); also offers the
+  compiled against third_party/eigen_subset (oracle/build_ref.sh); also offers the
   reference's input side (SMILES -> prepared ligand, build_pocket, codec).
 
 Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this.

@@ -3,7 +3,7 @@
 // ============================================================================
 // C entry points over the reference's OWN sources, compiled unchanged from
 // /root/reference/proj/src (see oracle/build_ref.sh) against the Eigen-subset
-// restatement in oracle/eigen_subset.  The output library lives in
+// restatement in third_party/eigen_subset.  The output library lives in
 // oracle/_ref/ (git-ignored, shipped to the GPU box by gpurun).  Entry points
 // mirror liboracle.so's vso_* so tests can compare the two line by line.
 #include <algorithm>

@@ -76,7 +76,7 @@ struct vs_context {
   // batch inputs
   DevBuf atom_off, bond_off, tors_off, ditem_base, xyz, elem, heavy, bond_a, bond_b, tors_bond, right_off, right_atoms;
   // derived
-  DevBuf meta, tmask, heavy_list, dmask, tors_ha, tors_hb, d_count, d_off, ditems;
+  DevBuf meta, tmask, heavy_list, dmask, tors_a, tors_b, d_count, d_off, ditems;
   // flatten / search / select
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
@@ -90,7 +90,8 @@ struct vs_pocket {
   double spacing = 0.5;
   int dims[3] = {0, 0, 0};
   int n_protein = 0;
-  DevBuf values, pxyz, pclass, cell_start, cell_atoms;
+  DevBuf values, pxyz, pclass, cell_start, cell_atoms, packed, palette;
+  int packed_mode = 0;
   double cmin[3] = {0, 0, 0};
   double cs = 2.0;
   int cdims[3] = {0, 0, 0};
@@ -121,6 +122,13 @@ struct vs_pocket {
     p.cs = cs;
     p.cell_start = has_cells ? cell_start.as<int>() : nullptr;
     p.cell_atoms = has_cells ? cell_atoms.as<int>() : nullptr;
+    p.packed.mode = packed_mode;
+    p.packed.cx = dims[0] - 1;
+    p.packed.cy = dims[1] - 1;
+    p.packed.c2 = packed_mode == 1 ? packed.as<uint16_t>() : nullptr;
+    p.packed.c4 = packed_mode == 2 ? packed.as<uint32_t>() : nullptr;
+    p.packed.inv_h = 1.0 / spacing;  // correctly rounded reciprocal for div_h
+    p.palette = palette.as<double>();
     return p;
   }
 };
@@ -193,6 +201,60 @@ vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
   CUDA_TRY(cudaMemcpy(p->cell_start.p, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->cell_atoms.p, atoms.data(), atoms.size() * sizeof(int), cudaMemcpyHostToDevice));
   p->has_cells = true;
+  return VS_OK;
+}
+
+// Cell-packed palette grid for the search sampler (dmath.cuh): when the node
+// values take at most 4 (16) distinct doubles, each cell's 8 corner codes fit
+// in one 16-bit (32-bit) word.  Values are reproduced exactly via the palette.
+vs_status build_packed(vs_pocket *p, const double *values) {
+  std::vector<double> pal;
+  const size_t nv = static_cast<size_t>(p->dims[0]) * p->dims[1] * p->dims[2];
+  std::vector<uint8_t> code(nv);
+  for (size_t i = 0; i < nv && pal.size() <= 16; ++i) {
+    const double v = values[i];
+    size_t c = 0;
+    uint64_t vb, pb;
+    std::memcpy(&vb, &v, 8);
+    for (; c < pal.size(); ++c) {
+      std::memcpy(&pb, &pal[c], 8);
+      if (pb == vb) break;  // bitwise identity keeps -0.0 / NaN payloads exact
+    }
+    if (c == pal.size()) pal.push_back(v);
+    code[i] = static_cast<uint8_t>(c);
+  }
+  p->packed_mode = pal.size() <= 4 ? 1 : (pal.size() <= 16 ? 2 : 0);
+  std::vector<double> pal16(16, 0.0);
+  for (size_t c = 0; c < pal.size() && c < 16; ++c) pal16[c] = pal[c];
+  CUDA_TRY(p->palette.ensure(sizeof(double) * 16));
+  CUDA_TRY(cudaMemcpy(p->palette.p, pal16.data(), sizeof(double) * 16, cudaMemcpyHostToDevice));
+  if (p->packed_mode == 0) return VS_OK;
+  const int cx = p->dims[0] - 1, cy = p->dims[1] - 1, cz = p->dims[2] - 1;
+  const size_t ncell = static_cast<size_t>(cx) * cy * cz;
+  const int bits = p->packed_mode == 1 ? 2 : 4;
+  std::vector<uint32_t> words(ncell, 0u);
+  for (int iz = 0; iz < cz; ++iz)
+    for (int iy = 0; iy < cy; ++iy)
+      for (int ix = 0; ix < cx; ++ix) {
+        uint32_t w = 0;
+        for (int c = 0; c < 8; ++c) {
+          const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+          const size_t node = static_cast<size_t>(ix + dx) +
+                              static_cast<size_t>(p->dims[0]) * (static_cast<size_t>(iy + dy) +
+                                                                 static_cast<size_t>(p->dims[1]) * (iz + dz));
+          w |= static_cast<uint32_t>(code[node]) << (bits * c);
+        }
+        words[static_cast<size_t>(ix) + static_cast<size_t>(cx) * (static_cast<size_t>(iy) + static_cast<size_t>(cy) * iz)] = w;
+      }
+  if (p->packed_mode == 1) {
+    std::vector<uint16_t> w16(ncell);
+    for (size_t i = 0; i < ncell; ++i) w16[i] = static_cast<uint16_t>(words[i]);
+    CUDA_TRY(p->packed.ensure(sizeof(uint16_t) * ncell));
+    CUDA_TRY(cudaMemcpy(p->packed.p, w16.data(), sizeof(uint16_t) * ncell, cudaMemcpyHostToDevice));
+  } else {
+    CUDA_TRY(p->packed.ensure(sizeof(uint32_t) * ncell));
+    CUDA_TRY(cudaMemcpy(p->packed.p, words.data(), sizeof(uint32_t) * ncell, cudaMemcpyHostToDevice));
+  }
   return VS_OK;
 }
 
@@ -280,8 +342,8 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   CUDA_TRY(ctx->tmask.ensure(4 * na));
   CUDA_TRY(ctx->heavy_list.ensure(2 * na));
   CUDA_TRY(ctx->dmask.ensure(4 * na));
-  CUDA_TRY(ctx->tors_ha.ensure(2 * nt));
-  CUDA_TRY(ctx->tors_hb.ensure(2 * nt));
+  CUDA_TRY(ctx->tors_a.ensure(2 * nt));
+  CUDA_TRY(ctx->tors_b.ensure(2 * nt));
   CUDA_TRY(ctx->d_count.ensure(4 * nt));
   CUDA_TRY(ctx->d_off.ensure(4 * nt));
   CUDA_TRY(ctx->ditems.ensure(2 * static_cast<size_t>(std::max(dbase, 1))));
@@ -303,8 +365,8 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   b.atom_tmask = ctx->tmask.as<uint32_t>();
   b.heavy_list = ctx->heavy_list.as<uint16_t>();
   b.heavy_dmask = ctx->dmask.as<uint32_t>();
-  b.tors_ha = ctx->tors_ha.as<uint16_t>();
-  b.tors_hb = ctx->tors_hb.as<uint16_t>();
+  b.tors_a = ctx->tors_a.as<uint16_t>();
+  b.tors_b = ctx->tors_b.as<uint16_t>();
   b.d_count = ctx->d_count.as<int>();
   b.d_off = ctx->d_off.as<int>();
   b.ditems = ctx->ditems.as<uint16_t>();
@@ -552,6 +614,7 @@ vs_status vs_pocket_create(vs_context *ctx, const vs_pocket_desc *d, vs_pocket *
   if (p->values.ensure(sizeof(double) * nv) != cudaSuccess ||
       cudaMemcpy(p->values.p, d->values, sizeof(double) * nv, cudaMemcpyHostToDevice) != cudaSuccess)
     rc = fail(VS_ERR_CUDA, "pocket grid upload failed");
+  if (rc == VS_OK) rc = build_packed(p, d->values);
   if (rc == VS_OK) rc = upload_protein(p, d->n_protein, d->protein_element, d->protein_xyz);
   if (rc != VS_OK) {
     delete p;
@@ -594,6 +657,13 @@ vs_status vs_pocket_build(vs_context *ctx, int32_t n, const uint8_t *elem, const
                                              dim, dim, p->values.as<double>(), ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) rc = fail(VS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (rc == VS_OK) {
+    std::vector<double> vals(nv);
+    if (cudaMemcpy(vals.data(), p->values.p, sizeof(double) * nv, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = fail(VS_ERR_CUDA, "pocket grid download failed");
+    else
+      rc = build_packed(p, vals.data());
   }
   if (rc == VS_OK) rc = upload_protein(p, n, elem, xyz);
   if (rc != VS_OK) {

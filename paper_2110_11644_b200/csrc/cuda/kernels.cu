@@ -29,7 +29,10 @@ __constant__ double c_lattice_sc[72];
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
-void set_lattice_table(const double *sc72) { cudaMemcpyToSymbol(c_lattice_sc, sc72, sizeof(double) * 72); }
+void set_lattice_table(const double *sc72) {
+  cudaMemcpyToSymbol(c_lattice_sc, sc72, sizeof(double) * 72);
+  set_lattice_table_search(sc72);
+}
 
 __device__ __forceinline__ d3 ld3(const double *p) { return {p[0], p[1], p[2]}; }
 __device__ __forceinline__ void st3(double *p, d3 v) {
@@ -88,22 +91,10 @@ __global__ void k_setup(batch_dev b, int restarts) {
       meta.r_all += 1;
       meta.r_heavy += b.heavy[a0 + b.right_atoms[r]] ? 1 : 0;
     }
-  // Heavy index of each torsion endpoint (the search tracks heavy atoms).
   for (int t = 0; t < m; ++t) {
     const int bi = b.tors_bond[t0 + t];
-    const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
-    int ha = -1, hb = -1;
-    for (int h = 0; h < n; ++h) {
-      if (b.heavy_list[a0 + h] == ea) ha = h;
-      if (b.heavy_list[a0 + h] == eb) hb = h;
-    }
-    if (ha < 0 || hb < 0) {  // hydrogen torsion endpoint: not produced by detect_torsions
-      meta.status = VS_LIG_TOO_LARGE;
-      b.meta[l] = meta;
-      return;
-    }
-    b.tors_ha[t0 + t] = (uint16_t)ha;
-    b.tors_hb[t0 + t] = (uint16_t)hb;
+    b.tors_a[t0 + t] = b.bond_a[b0 + bi];
+    b.tors_b[t0 + t] = b.bond_b[b0 + bi];
   }
   // D_t: atoms whose coordinates can depend on torsion t's angle.  Start
   // from right_set(t); a later torsion u joins when either endpoint is
@@ -114,7 +105,7 @@ __global__ void k_setup(batch_dev b, int restarts) {
   for (int t = 0; t < m; ++t) {
     uint32_t dset = 1u << t;  // torsions whose right sets are in D_t
     for (int u = t + 1; u < m; ++u) {
-      const int ea = b.heavy_list[a0 + b.tors_ha[t0 + u]], eb = b.heavy_list[a0 + b.tors_hb[t0 + u]];
+      const int ea = b.tors_a[t0 + u], eb = b.tors_b[t0 + u];
       if ((b.atom_tmask[a0 + ea] & dset) || (b.atom_tmask[a0 + eb] & dset)) dset |= 1u << u;
     }
     int cnt = 0;
@@ -305,480 +296,6 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
   cudaFuncSetAttribute(k_flatten, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_flatten<<<b.n_lig, kFlatThreads, smem, s>>>(b, max_sweeps, f, cb);
   return cudaGetLastError();
-}
-
-// ============================================================== k_search
-// One warp per (ligand, restart).  Per-warp shared memory (doubles):
-//   conf[N*3]  current pose, all atoms (pivot = its centroid)
-//   tors[N*3]  torsioned, untransformed frame (search.cpp:115)
-//   P[m*n*3]   heavy-atom prefix states: P_t = atoms before torsion t
-//   Mcur[m*12] current torsion matrices {R, pivot}
-//   Mvar[2m*m*12] torsion-neighbour matrices (only u >= t used)
-//   Rj[12*16]  rigid neighbours {R, t, q}
-//   vb[J*n]    per-neighbour, per-heavy-atom field values
-//   vcur[n]    field values of the current pose
-//   scores[J], cache[2m*2] (sin,cos of cur +- step), ang[m], sccur[m*2]
-//   state[32]  q, t, R, pivot, geo, steps
-//   dm[n] (u32), cvalid[2m] (int)
-struct search_args {
-  batch_dev b;
-  pocket_dev p;
-  search_cfg c;
-  flat_out f;
-  item_out o;
-  const double *pose_in;   // local_search mode: [items][8] q,t,geo; NULL in dock mode
-  const double *ang_in;    // local_search mode: per torsion
-  const double *conf_in;   // local_search mode: 3*atoms
-  int *work;
-  int n_items;
-  int Nmax, nmax, mmax, Jmax;
-  int warp_doubles;
-  int o_conf, o_tors, o_P, o_Mcur, o_Mvar, o_Rj, o_vb, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_dm,
-      o_cvalid;
-};
-
-enum { S_Q = 0, S_T = 4, S_R = 7, S_PIV = 16, S_GEO = 19, S_STEPT = 20, S_STEPR = 21, S_STEPQ = 22, S_ERR = 23, S_N = 24 };
-
-// Matrices of torsions u = t..m-1 for a pose whose angles equal the current
-// ones except torsion t (sin/cos st/ct): each endpoint is carried from the
-// prefix P_t through the already-built rotations (per-atom composition of
-// apply_torsions, transform.cpp:73-81).  Single lane.
-__device__ bool chain_mats(int t, double st, double ct, int m, const double *P, int nmax, const uint16_t *ha,
-                           const uint16_t *hb, const uint16_t *hl, const uint32_t *tm, const double *sccur, double *out) {
-  for (int u = t; u < m; ++u) {
-    const int hA = ha[u], hB = hb[u];
-    d3 ea = ld3(P + 3 * (t * nmax + hA));
-    d3 eb = ld3(P + 3 * (t * nmax + hB));
-    const uint32_t ma = tm[hl[hA]], mb = tm[hl[hB]];
-    for (int w = t; w < u; ++w) {
-      if ((ma >> w) & 1u) ea = torsion_apply(out + 12 * w, ea);
-      if ((mb >> w) & 1u) eb = torsion_apply(out + 12 * w, eb);
-    }
-    const double s = u == t ? st : sccur[2 * u];
-    const double c = u == t ? ct : sccur[2 * u + 1];
-    if (!torsion_setup(ea, eb, s, c, out + 12 * u)) return false;
-  }
-  return true;
-}
-
-// Rebuild P (heavy prefixes) and tors (all atoms) from the base coordinates
-// with the current matrices Mcur.  Warp-cooperative over atoms.
-__device__ __forceinline__ void rebuild_frames(int lane, int N, int m, int nmax, const double *base, const uint8_t *heavy,
-                                               const uint32_t *tm, const double *Mcur, double *P, double *tors,
-                                               const int *heavy_index) {
-  for (int a = lane; a < N; a += 32) {
-    d3 x = ld3(base + 3 * a);
-    const int h = heavy_index[a];
-    const uint32_t mask = tm[a];
-    for (int u = 0; u < m; ++u) {
-      if (h >= 0) st3(P + 3 * (u * nmax + h), x);
-      if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
-    }
-    st3(tors + 3 * a, x);
-  }
-  (void)heavy;
-}
-
-__global__ void __launch_bounds__(128) k_search(search_args A) {
-  extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  double *W = sm + (size_t)warp * A.warp_doubles;
-  double *conf = W + A.o_conf;
-  double *tors = W + A.o_tors;
-  double *P = W + A.o_P;
-  double *Mcur = W + A.o_Mcur;
-  double *Mvar = W + A.o_Mvar;
-  double *Rj = W + A.o_Rj;
-  double *vb = W + A.o_vb;
-  double *vcur = W + A.o_vcur;
-  double *scores = W + A.o_scores;
-  double *cache = W + A.o_cache;
-  double *ang = W + A.o_ang;
-  double *sccur = W + A.o_sccur;
-  double *S = W + A.o_state;
-  uint32_t *dm = reinterpret_cast<uint32_t *>(W + A.o_dm);
-  int *cvalid = reinterpret_cast<int *>(W + A.o_cvalid);
-  // heavy index of each atom (-1 for hydrogens) lives after cvalid
-  int *hidx = cvalid + 2 * A.mmax + 2;
-
-  const batch_dev &b = A.b;
-  const grid_view &g = A.p.g;
-  const int k = A.pose_in ? 1 : A.c.k;
-  const int nmax = A.nmax;
-
-  while (true) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(A.work, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= A.n_items) break;
-    const int l = item / k, r = item - l * k;
-    const lig_meta meta = b.meta[l];
-    if (meta.status != VS_LIG_OK) {
-      if (lane == 0) A.o.status[item] = meta.status;
-      continue;
-    }
-    const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
-    const int a0 = b.atom_off[l], t0 = b.tors_off[l];
-    const double *base = b.xyz + 3 * (size_t)a0;
-    const uint16_t *hl = b.heavy_list + a0;
-    const uint32_t *tm = b.atom_tmask + a0;
-    const uint16_t *ha = b.tors_ha + t0, *hb = b.tors_hb + t0;
-    const int *dcnt = b.d_count + t0, *doff = b.d_off + t0;
-    const uint16_t *ditems = b.ditems + b.ditem_base[l];
-    const int J = 12 + 2 * m;
-    unsigned long long evals = 0;
-
-    // ---- per-ligand tables into shared memory
-    for (int a = lane; a < N; a += 32) hidx[a] = -1;
-    __syncwarp();
-    for (int h = lane; h < n; h += 32) {
-      hidx[hl[h]] = h;
-      dm[h] = b.heavy_dmask[a0 + h];
-    }
-    for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
-    if (A.pose_in) {
-      for (int u = lane; u < m; u += 32) {
-        ang[u] = A.ang_in[t0 + u];
-        vs_crtrig::sincos_cr(ang[u], &sccur[2 * u], &sccur[2 * u + 1]);
-      }
-    } else {
-      for (int u = lane; u < m; u += 32) {
-        const int li = A.f.idx[t0 + u];
-        ang[u] = li * kLatticeStep;
-        sccur[2 * u] = c_lattice_sc[2 * li];
-        sccur[2 * u + 1] = c_lattice_sc[2 * li + 1];
-      }
-    }
-    for (int h = lane; h < n; h += 32) st3(P + 3 * h, ld3(base + 3 * hl[h]));  // P_0 = base
-    __syncwarp();
-    if (lane == 0) {
-      S[S_ERR] = 0.0;
-      if (m > 0 && !chain_mats(0, sccur[0], sccur[1], m, P, nmax, ha, hb, hl, tm, sccur, Mcur)) S[S_ERR] = 1.0;
-    }
-    __syncwarp();
-    if (S[S_ERR] != 0.0) {
-      if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
-      continue;
-    }
-    rebuild_frames(lane, N, m, nmax, base, nullptr, tm, Mcur, P, tors, hidx);
-    __syncwarp();
-
-    // ---- initial pose (initial_poses, search.cpp:95-103) or the given one
-    if (lane == 0) {
-      quat q;
-      double t[3];
-      if (A.pose_in) {
-        const double *pi = A.pose_in + 8 * l;
-        q = {pi[0], pi[1], pi[2], pi[3]};
-        t[0] = pi[4];
-        t[1] = pi[5];
-        t[2] = pi[6];
-      } else {
-        const double *fq = A.c.fibq + 4 * r;
-        q = {fq[0], fq[1], fq[2], fq[3]};
-        const d3 fc = ld3(A.f.centroid + 3 * l);
-        const d3 rc = quat_rotate(q, fc);
-        t[0] = A.p.center[0] - rc.x;
-        t[1] = A.p.center[1] - rc.y;
-        t[2] = A.p.center[2] - rc.z;
-      }
-      S[S_Q] = q.x;
-      S[S_Q + 1] = q.y;
-      S[S_Q + 2] = q.z;
-      S[S_Q + 3] = q.w;
-      S[S_T] = t[0];
-      S[S_T + 1] = t[1];
-      S[S_T + 2] = t[2];
-      quat_matrix(q, S + S_R);
-    }
-    __syncwarp();
-    // current-pose sample values from apply_rigid(tors, T)
-    for (int h = lane; h < n; h += 32) {
-      const int a = hl[h];
-      bool out;
-      vcur[h] = field_value(g, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a), out);
-    }
-    if (A.pose_in) {
-      const double *ci = A.conf_in + 3 * (size_t)a0;
-      for (int i = lane; i < 3 * N; i += 32) conf[i] = ci[i];
-    } else {
-      for (int a = lane; a < N; a += 32) st3(conf + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
-    }
-    __syncwarp();
-    if (lane == 0) {
-      if (A.pose_in) {
-        S[S_GEO] = A.pose_in[8 * l + 7];
-      } else {
-        double acc = 0.0;
-        for (int h = 0; h < n; ++h) acc += vcur[h];
-        S[S_GEO] = acc;
-      }
-      S[S_STEPT] = A.c.step_t;
-      S[S_STEPR] = A.c.step_r;
-      S[S_STEPQ] = A.c.step_q;
-    }
-    if (!A.pose_in) evals += (unsigned long long)n;
-    __syncwarp();
-
-    // ---- local_search (search.cpp:121-191)
-    int level = 0, n_iter = 0, n_adopt = 0;
-    bool failed = false;
-    for (int iter = 0; iter < A.c.max_iter && S[S_STEPT] >= A.c.min_t; ++iter) {
-      if (lane < 3) S[S_PIV + lane] = centroid_row(conf, N, lane);
-      __syncwarp();
-      const double step_t = S[S_STEPT], step_q = S[S_STEPQ];
-      for (int w = lane; w < J; w += 32) {
-        if (w < 12) {
-          double *X = Rj + 16 * w;
-          if (w < 6) {  // translations (search.cpp:152-158)
-            const int axis = w >> 1;
-            const double sign = (w & 1) ? -1.0 : 1.0;
-            for (int q = 0; q < 9; ++q) X[q] = S[S_R + q];
-            for (int q = 0; q < 3; ++q) X[9 + q] = S[S_T + q];
-            X[9 + axis] = S[S_T + axis] + sign * step_t;
-            for (int q = 0; q < 4; ++q) X[12 + q] = S[S_Q + q];
-          } else {  // rotations about the pivot (search.cpp:159-167)
-            const double *sq = A.c.spin + 4 * (6 * level + (w - 6));
-            const quat spin{sq[0], sq[1], sq[2], sq[3]};
-            const d3 piv = ld3(S + S_PIV);
-            const d3 sp = quat_rotate(spin, piv);
-            const d3 spin_t = sub3(piv, sp);
-            const quat cur{S[S_Q], S[S_Q + 1], S[S_Q + 2], S[S_Q + 3]};
-            const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
-            const d3 tt = add3(quat_rotate(spin, ld3(S + S_T)), spin_t);
-            quat_matrix(qn, X);
-            X[9] = tt.x;
-            X[10] = tt.y;
-            X[11] = tt.z;
-            X[12] = qn.x;
-            X[13] = qn.y;
-            X[14] = qn.z;
-            X[15] = qn.w;
-          }
-        } else {  // torsion neighbours (search.cpp:168-176)
-          const int v = w - 12, t = v >> 1;
-          const double sign = (v & 1) ? -1.0 : 1.0;
-          if (!cvalid[v]) {
-            const double a = ang[t] + sign * step_q;
-            vs_crtrig::sincos_cr(a, &cache[2 * v], &cache[2 * v + 1]);
-            cvalid[v] = 1;
-          }
-          if (!chain_mats(t, cache[2 * v], cache[2 * v + 1], m, P, nmax, ha, hb, hl, tm, sccur,
-                          Mvar + (size_t)12 * A.mmax * v))
-            S[S_ERR] = 1.0;
-        }
-      }
-      __syncwarp();
-      if (S[S_ERR] != 0.0) {
-        failed = true;
-        break;
-      }
-      // neighbour x heavy-atom samples
-      int total_d = 0;
-      for (int t = 0; t < m; ++t) total_d += dcnt[t];
-      const int nR = 12 * n, nT = 2 * total_d;
-      for (int it = lane; it < nR + nT; it += 32) {
-        if (it < nR) {
-          const int j = it / n, h = it - j * n;
-          const int a = hl[h];
-          const double *X = Rj + 16 * j;
-          bool out;
-          vb[j * nmax + h] = field_value(g, rigid_col(X, X + 9, ld3(tors + 3 * a), a), out);
-        } else {
-          const int kk = it - nR;
-          int t = 0;
-          while (kk >= 2 * (doff[t] + dcnt[t])) ++t;
-          const int rem = kk - 2 * doff[t];
-          const int s = rem >= dcnt[t] ? 1 : 0;
-          const int h = ditems[doff[t] + rem - s * dcnt[t]];
-          const int v = 2 * t + s;
-          const int a = hl[h];
-          const double *Mv = Mvar + (size_t)12 * A.mmax * v;
-          d3 x = ld3(P + 3 * (t * nmax + h));
-          const uint32_t mask = tm[a];
-          for (int u = t; u < m; ++u)
-            if ((mask >> u) & 1u) x = torsion_apply(Mv + 12 * u, x);
-          bool out;
-          vb[(12 + v) * nmax + h] = field_value(g, rigid_col(S + S_R, S + S_T, x, a), out);
-        }
-      }
-      __syncwarp();
-      // geo_score of each neighbour: sequential over heavy atoms (grid.cpp:97-101)
-      for (int j = lane; j < J; j += 32) {
-        double acc = 0.0;
-        const double *row = vb + j * nmax;
-        if (j < 12) {
-          for (int h = 0; h < n; ++h) acc += row[h];
-        } else {
-          const int t = (j - 12) >> 1;
-          for (int h = 0; h < n; ++h) acc += ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
-        }
-        scores[j] = acc;
-      }
-      evals += (unsigned long long)n * J;
-      __syncwarp();
-      // strict-best neighbour, first wins on ties (search.cpp:138)
-      double bv = -__longlong_as_double(0x7ff0000000000000LL);
-      int bj = 0x7fffffff;
-      for (int j = lane; j < J; j += 32)
-        if (scores[j] > bv) {
-          bv = scores[j];
-          bj = j;
-        }
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
-        if (ov > bv || (ov == bv && oj < bj)) {
-          bv = ov;
-          bj = oj;
-        }
-      }
-      const bool improved = bv > S[S_GEO];
-      ++n_iter;
-      n_adopt += improved ? 1 : 0;
-      __syncwarp();
-      if (improved) {
-        if (bj < 12) {
-          const double *X = Rj + 16 * bj;
-          if (lane < 9) S[S_R + lane] = X[lane];
-          else if (lane < 12) S[S_T + lane - 9] = X[lane];
-          else if (lane < 16) S[S_Q + lane - 12] = X[lane];
-          __syncwarp();
-          for (int a = lane; a < N; a += 32) st3(conf + 3 * a, rigid_col(X, X + 9, ld3(tors + 3 * a), a));
-          for (int h = lane; h < n; h += 32) vcur[h] = vb[bj * nmax + h];
-        } else {
-          const int v = bj - 12, t = v >> 1;
-          const double sign = (v & 1) ? -1.0 : 1.0;
-          const double *Mv = Mvar + (size_t)12 * A.mmax * v;
-          for (int i = lane; i < 12 * (m - t); i += 32) Mcur[12 * t + i] = Mv[12 * t + i];
-          if (lane == 0) {
-            ang[t] = ang[t] + sign * step_q;
-            sccur[2 * t] = cache[2 * v];
-            sccur[2 * t + 1] = cache[2 * v + 1];
-            cvalid[2 * t] = 0;
-            cvalid[2 * t + 1] = 0;
-          }
-          __syncwarp();
-          rebuild_frames(lane, N, m, nmax, base, nullptr, tm, Mcur, P, tors, hidx);
-          __syncwarp();
-          for (int a = lane; a < N; a += 32)
-            st3(conf + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
-          for (int h = lane; h < n; h += 32)
-            if ((dm[h] >> t) & 1u) vcur[h] = vb[bj * nmax + h];
-        }
-        if (lane == 0) S[S_GEO] = bv;
-      } else {
-        if (lane == 0) {
-          S[S_STEPT] = S[S_STEPT] * 0.5;
-          S[S_STEPR] = S[S_STEPR] * 0.5;
-          S[S_STEPQ] = S[S_STEPQ] * 0.5;
-        }
-        for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
-        ++level;
-      }
-      __syncwarp();
-    }
-    if (failed) {
-      if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
-      continue;
-    }
-    // ---- outputs
-    const size_t ck = (size_t)a0 * k + (size_t)r * N;
-    for (int i = lane; i < 3 * N; i += 32) A.o.conf[3 * ck + i] = conf[i];
-    const size_t tk = (size_t)t0 * k + (size_t)r * m;
-    for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = ang[u];
-    if (lane < 4) A.o.T[7 * (size_t)item + lane] = S[S_Q + lane];
-    else if (lane < 7) A.o.T[7 * (size_t)item + lane] = S[S_T + lane - 4];
-    if (lane == 0) {
-      A.o.geo[item] = S[S_GEO];
-      A.o.evals[item] = evals;
-      A.o.status[item] = VS_LIG_OK;
-      if (A.o.iters) A.o.iters[item] = n_iter;
-      if (A.o.adopts) A.o.adopts[item] = n_adopt;
-    }
-    __syncwarp();
-  }
-}
-
-static cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
-  const int Nm = A.Nmax, nm = A.nmax, mm = A.mmax, Jm = 12 + 2 * mm;
-  A.Jmax = Jm;
-  int o = 0;
-  auto take = [&](int n) {
-    const int at = o;
-    o += (n + 1) & ~1;  // keep 16-byte alignment
-    return at;
-  };
-  A.o_conf = take(3 * Nm);
-  A.o_tors = take(3 * Nm);
-  A.o_P = take(3 * mm * nm);
-  A.o_Mcur = take(12 * mm);
-  A.o_Mvar = take(12 * mm * 2 * mm);
-  A.o_Rj = take(16 * 12);
-  A.o_vb = take(Jm * nm);
-  A.o_vcur = take(nm);
-  A.o_scores = take(Jm);
-  A.o_cache = take(4 * mm);
-  A.o_ang = take(mm);
-  A.o_sccur = take(2 * mm);
-  A.o_state = take(S_N);
-  A.o_dm = take((nm + 1) / 2);
-  A.o_cvalid = take((2 * mm + 2 + Nm + 1) / 2 + 1);
-  A.warp_doubles = o;
-  const int warps = 4;
-  const size_t smem = (size_t)o * sizeof(double) * warps;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32 * warps, smem);
-  if (per_sm < 1) per_sm = 1;
-  int blocks = num_sms * per_sm;
-  const int need = (A.n_items + warps - 1) / warps;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  k_search<<<blocks, 32 * warps, smem, s>>>(A);
-  if (launches) ++*launches;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
-                          const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
-                          int num_sms, cudaStream_t s, int *launches) {
-  search_args A{};
-  A.b = b;
-  A.p = p;
-  A.c = c;
-  A.f = f;
-  A.o = o;
-  A.work = work_counter;
-  A.n_items = b.n_lig * c.k;
-  A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
-  A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
-  A.mmax = mmax > 0 ? mmax : 1;
-  if (A.n_items == 0) return cudaSuccess;
-  return run_search(A, num_sms, s, launches);
-}
-
-cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,
-                                const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,
-                                int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s) {
-  search_args A{};
-  A.b = b;
-  A.p = p;
-  A.c = c;
-  A.o = o;
-  A.pose_in = pose_in;
-  A.ang_in = ang_in;
-  A.conf_in = conf_in;
-  A.work = work_counter;
-  A.n_items = b.n_lig;
-  A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
-  A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
-  A.mmax = mmax > 0 ? mmax : 1;
-  if (A.n_items == 0) return cudaSuccess;
-  return run_search(A, num_sms, s, nullptr);
 }
 
 // ============================================================== chem

@@ -40,8 +40,8 @@ struct batch_dev {
   uint32_t *atom_tmask;    // atoms: bit t <=> atom in right_set(t)
   uint16_t *heavy_list;    // atoms capacity: local atom index of heavy h
   uint32_t *heavy_dmask;   // atoms capacity: bit t <=> heavy h in D_t
-  uint16_t *tors_ha;       // torsions: heavy index of bond.a
-  uint16_t *tors_hb;       // torsions: heavy index of bond.b
+  uint16_t *tors_a;        // torsions: local atom index of bond.a (pivot)
+  uint16_t *tors_b;        // torsions: local atom index of bond.b
   int *d_count;            // torsions: |D_t ∩ heavy|
   int *d_off;              // torsions: offset of D_t items in the ligand list
   uint16_t *ditems;        // ditem_base[l] + ...: heavy indices of D_t items
@@ -49,6 +49,8 @@ struct batch_dev {
 
 struct pocket_dev {
   grid_view g;
+  packed_grid packed;       // cell-packed palette codes for the search sampler
+  const double *palette;    // 16 values (device)
   double center[3];
   int n_protein;
   const double *pxyz;       // 3*P
@@ -101,6 +103,7 @@ struct dock_out {
 };
 
 void set_lattice_table(const double *sc72);
+void set_lattice_table_search(const double *sc72);
 
 cudaError_t launch_setup(const batch_dev &b, int restarts, cudaStream_t s);
 cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,

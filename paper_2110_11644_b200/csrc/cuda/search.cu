@@ -1,0 +1,599 @@
+// k_search: initial_poses + local_search (search.cpp:84-193) on sm_100a.
+//
+// One warp owns one (ligand, restart) work item; warps pull items from a
+// global atomic counter (persistent grid, CTAs of 4 warps, as many CTAs per
+// SM as registers and shared memory allow).  Per local_search iteration the
+// warp evaluates the 12 + 2m neighbours of search.cpp:152-176:
+//
+//   * neighbour x heavy-atom samples are flattened into one item list and
+//     spread over the 32 lanes (rigid neighbours: every heavy atom; torsion
+//     neighbour (t, +-): only the heavy atoms of D_t, the atoms whose
+//     coordinates can depend on torsion t -- every other atom follows a
+//     bit-identical trajectory, so its sample equals the current pose's);
+//   * each neighbour's geo_score is then summed by one lane in heavy-atom
+//     order (grid.cpp:97-101), reading the per-atom values back from shared
+//     memory -- the reference's sequential double sum, bit for bit;
+//   * the strictly best neighbour (first wins on ties, search.cpp:138) is a
+//     warp shuffle reduction over the scores.
+//
+// The neighbourhood is processed in groups of at most G neighbours (rigid
+// group first, then torsion groups in order), keeping a running best, so the
+// per-warp buffer holds G rows instead of 12 + 2m.  Torsion-neighbour
+// matrices depend only on the torsion state and the step, so they are
+// rebuilt only after a torsion move or a step halving; the pivot only after
+// a move.  All arithmetic is FP64 in the reference's evaluation order.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../../include/vs_crtrig.h"
+#include "../../../include/vs_dock.h"
+#include "kernels.cuh"
+
+namespace vsd {
+
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kGroup = 16;  // neighbours per group (>= 12)
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kLatticeStep = 2.0 * kPi / 36;
+
+__device__ __forceinline__ d3 ld3(const double *p) { return {p[0], p[1], p[2]}; }
+__device__ __forceinline__ void st3(double *p, d3 v) {
+  p[0] = v.x;
+  p[1] = v.y;
+  p[2] = v.z;
+}
+
+// Row `row` of rigid_col (the reference's 3xN apply_rigid, Appendix A item 4).
+__device__ __forceinline__ double rigid_row(const double *r, const double *t, d3 v, int col, int row) {
+  const double a0 = r[3 * row] * v.x, a1 = r[3 * row + 1] * v.y, a2 = r[3 * row + 2] * v.z;
+  const bool packet = (col & 1) == 0 ? row < 2 : row > 0;
+  return (packet ? (a0 + a1) + a2 : a0 + (a1 + a2)) + t[row];
+}
+
+__device__ __noinline__ void sincos_cr_dev(double a, double *s, double *c) { vs_crtrig::sincos_cr(a, s, c); }
+
+__constant__ double c_lattice_sc_s[72];
+__device__ __forceinline__ double c_lattice_sc_dev(int i) { return c_lattice_sc_s[i]; }
+
+enum {
+  S_Q = 0,      // current rotation (x, y, z, w)
+  S_T = 4,      // current translation
+  S_R = 7,      // current rotation matrix
+  S_PIV = 16,   // pivot
+  S_GEO = 19,   // current geo_score
+  S_STEPT = 20,
+  S_STEPR = 21,
+  S_STEPQ = 22,
+  S_ERR = 23,
+  S_N = 24
+};
+
+}  // namespace
+
+struct search_args {
+  batch_dev b;
+  pocket_dev p;
+  packed_grid pg;
+  search_cfg c;
+  flat_out f;
+  item_out o;
+  const double *pose_in;  // local_search mode: [n][8] q, t, geo; NULL in dock mode
+  const double *ang_in;
+  const double *conf_in;
+  int *work;
+  int n_items;
+  int Nmax, nmax, mmax;
+  int warp_doubles;
+  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints;
+};
+
+// Offset (in doubles) of variant v's matrix for torsion u >= t(v) inside the
+// triangular Mvar block: variants (t, +), (t, -) each hold m - t matrices.
+__device__ __forceinline__ int mvar_off(int v, int u, int m) {
+  const int t = v >> 1, s = v & 1;
+  return 12 * (2 * (t * m - (t * (t - 1)) / 2) + s * (m - t) + (u - t));
+}
+
+// Matrices of torsions t..m-1 for the pose whose angles equal the current
+// ones except torsion t (sin/cos st, ct); endpoints are carried from the
+// base coordinates through the current matrices (u' < t) and the new ones
+// (t <= u' < u): the per-atom composition of apply_torsions
+// (transform.cpp:73-81).  Single lane.  out(u) = out + 12 * (u - t).
+__device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, const double *base, const uint16_t *ta,
+                                        const uint16_t *tb, const uint32_t *tm, const double *Mcur,
+                                        const double *sccur, double *out) {
+  for (int u = t; u < m; ++u) {
+    const int a = ta[u], b = tb[u];
+    d3 ea = ld3(base + 3 * a), eb = ld3(base + 3 * b);
+    const uint32_t ma = tm[a], mb = tm[b];
+    for (int w = 0; w < u; ++w) {
+      const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
+      if ((ma >> w) & 1u) ea = torsion_apply(M, ea);
+      if ((mb >> w) & 1u) eb = torsion_apply(M, eb);
+    }
+    const double s = u == t ? st : sccur[2 * u];
+    const double c = u == t ? ct : sccur[2 * u + 1];
+    if (!torsion_setup(ea, eb, s, c, out + 12 * (u - t))) return false;
+  }
+  return true;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
+  extern __shared__ double sm[];
+  double *pal = sm;  // 16 palette values (CTA-wide)
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x < 16) pal[threadIdx.x] = MODE == 0 ? 0.0 : A.p.palette[threadIdx.x];
+  __syncthreads();
+  double *W = sm + 16 + (size_t)warp * A.warp_doubles;
+  double *tors = W + A.o_tors;
+  double *Mcur = W + A.o_Mcur;
+  double *Mvar = W + A.o_Mvar;
+  double *Rj = W + A.o_Rj;
+  double *vb = W + A.o_vb;
+  double *vbest = W + A.o_vbest;
+  double *vcur = W + A.o_vcur;
+  double *scores = W + A.o_scores;
+  double *cache = W + A.o_cache;
+  double *ang = W + A.o_ang;
+  double *sccur = W + A.o_sccur;
+  double *S = W + A.o_state;
+  uint32_t *dm = reinterpret_cast<uint32_t *>(W + A.o_ints);
+  int *hidx = reinterpret_cast<int *>(dm + A.nmax);
+  int *cvalid = hidx + A.Nmax;
+
+  const batch_dev &b = A.b;
+  const grid_view &g = A.p.g;
+  const packed_grid &pg = A.pg;
+  const bool ls_mode = A.pose_in != nullptr;
+  const int k = ls_mode ? 1 : A.c.k;
+  const int nmax = A.nmax;
+
+  while (true) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(A.work, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= A.n_items) break;
+    const int l = item / k, r = item - l * k;
+    const lig_meta meta = b.meta[l];
+    if (meta.status != VS_LIG_OK) {
+      if (lane == 0) A.o.status[item] = meta.status;
+      continue;
+    }
+    const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
+    const int a0 = b.atom_off[l], t0 = b.tors_off[l];
+    const double *base = b.xyz + 3 * (size_t)a0;
+    const uint16_t *hl = b.heavy_list + a0;
+    const uint32_t *tm = b.atom_tmask + a0;
+    const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
+    const int *dcnt = b.d_count + t0, *doff = b.d_off + t0;
+    const uint16_t *ditems = b.ditems + b.ditem_base[l];
+    const int J = 12 + 2 * m;
+    unsigned long long evals = 0;
+
+    // ---- per-ligand tables
+    for (int a = lane; a < N; a += 32) hidx[a] = -1;
+    __syncwarp();
+    for (int h = lane; h < n; h += 32) {
+      hidx[hl[h]] = h;
+      dm[h] = b.heavy_dmask[a0 + h];
+    }
+    for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
+    if (ls_mode) {
+      for (int u = lane; u < m; u += 32) {
+        ang[u] = A.ang_in[t0 + u];
+        sincos_cr_dev(ang[u], &sccur[2 * u], &sccur[2 * u + 1]);
+      }
+    } else {
+      for (int u = lane; u < m; u += 32) {
+        const int li = A.f.idx[t0 + u];
+        ang[u] = li * kLatticeStep;  // angles_of, search.cpp:40
+        sccur[2 * u] = c_lattice_sc_dev(2 * li);
+        sccur[2 * u + 1] = c_lattice_sc_dev(2 * li + 1);
+      }
+    }
+    if (lane == 0) S[S_ERR] = 0.0;
+    __syncwarp();
+    if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, base, ta, tb, tm, Mcur, sccur, Mcur))
+      S[S_ERR] = 1.0;
+    __syncwarp();
+    if (S[S_ERR] != 0.0) {
+      if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
+      continue;
+    }
+    // torsioned frame (search.cpp:115)
+    for (int a = lane; a < N; a += 32) {
+      d3 x = ld3(base + 3 * a);
+      const uint32_t mask = tm[a];
+      for (int u = 0; u < m; ++u)
+        if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
+      st3(tors + 3 * a, x);
+    }
+    // ---- start pose: initial_poses (search.cpp:95-103) or the given one
+    if (lane == 0) {
+      quat q;
+      double t[3];
+      if (ls_mode) {
+        const double *pi = A.pose_in + 8 * l;
+        q = {pi[0], pi[1], pi[2], pi[3]};
+        t[0] = pi[4];
+        t[1] = pi[5];
+        t[2] = pi[6];
+      } else {
+        const double *fq = A.c.fibq + 4 * r;
+        q = {fq[0], fq[1], fq[2], fq[3]};
+        const d3 rc = quat_rotate(q, ld3(A.f.centroid + 3 * l));
+        t[0] = A.p.center[0] - rc.x;
+        t[1] = A.p.center[1] - rc.y;
+        t[2] = A.p.center[2] - rc.z;
+      }
+      S[S_Q] = q.x;
+      S[S_Q + 1] = q.y;
+      S[S_Q + 2] = q.z;
+      S[S_Q + 3] = q.w;
+      S[S_T] = t[0];
+      S[S_T + 1] = t[1];
+      S[S_T + 2] = t[2];
+      quat_matrix(q, S + S_R);
+      S[S_STEPT] = A.c.step_t;
+      S[S_STEPR] = A.c.step_r;
+      S[S_STEPQ] = A.c.step_q;
+    }
+    __syncwarp();
+    for (int h = lane; h < n; h += 32) {
+      const int a = hl[h];
+      bool out;
+      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a), out);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (ls_mode) {
+        S[S_GEO] = A.pose_in[8 * l + 7];
+      } else {
+        double acc = 0.0;
+        for (int h = 0; h < n; ++h) acc += vcur[h];
+        S[S_GEO] = acc;
+      }
+    }
+    if (!ls_mode) evals += (unsigned long long)n;
+    // pivot of the start pose: centroid of its conformation (search.cpp:124)
+    if (lane < 3) {
+      const int row = lane;
+      double p;
+      auto val = [&](int a) -> double {
+        if (ls_mode) return A.conf_in[3 * ((size_t)a0 + a) + row];
+        return rigid_row(S + S_R, S + S_T, ld3(tors + 3 * a), a, row);
+      };
+      p = val(0);
+      if (row < 2) {
+        const int size4 = (N - 1) & ~3;
+        int i = 1;
+        for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
+        for (; i < N; ++i) p = p + val(i);
+      } else {
+        for (int i = 1; i < N; ++i) p = p + val(i);
+      }
+      S[S_PIV + row] = p / (double)N;
+    }
+    __syncwarp();
+
+    // ---- local_search (search.cpp:121-191)
+    int level = 0, n_iter = 0, n_adopt = 0;
+    bool failed = false, mvar_valid = false, moved = false;
+    for (int iter = 0; iter < A.c.max_iter && S[S_STEPT] >= A.c.min_t; ++iter) {
+      const double step_t = S[S_STEPT], step_q = S[S_STEPQ];
+      // rigid neighbour transforms (lanes 0-11) and, when stale, the
+      // torsion-neighbour matrices (lanes 12..; one lane per neighbour)
+      for (int w = lane; w < (mvar_valid ? 12 : J); w += 32) {
+        if (w < 12) {
+          double *X = Rj + 16 * w;
+          if (w < 6) {  // translations (search.cpp:152-158)
+            const int axis = w >> 1;
+            const double sign = (w & 1) ? -1.0 : 1.0;
+            for (int q = 0; q < 9; ++q) X[q] = S[S_R + q];
+            for (int q = 0; q < 3; ++q) X[9 + q] = S[S_T + q];
+            X[9 + axis] = S[S_T + axis] + sign * step_t;
+            for (int q = 0; q < 4; ++q) X[12 + q] = S[S_Q + q];
+          } else {  // rotations about the pivot (search.cpp:159-167)
+            const double *sq = A.c.spin + 4 * (6 * level + (w - 6));
+            const quat spin{sq[0], sq[1], sq[2], sq[3]};
+            const d3 piv = ld3(S + S_PIV);
+            const d3 spin_t = sub3(piv, quat_rotate(spin, piv));
+            const quat cur{S[S_Q], S[S_Q + 1], S[S_Q + 2], S[S_Q + 3]};
+            const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
+            const d3 tt = add3(quat_rotate(spin, ld3(S + S_T)), spin_t);
+            quat_matrix(qn, X);
+            X[9] = tt.x;
+            X[10] = tt.y;
+            X[11] = tt.z;
+            X[12] = qn.x;
+            X[13] = qn.y;
+            X[14] = qn.z;
+            X[15] = qn.w;
+          }
+        } else {  // torsion neighbour matrices (search.cpp:168-176)
+          const int v = w - 12, t = v >> 1;
+          const double sign = (v & 1) ? -1.0 : 1.0;
+          if (!cvalid[v]) {
+            sincos_cr_dev(ang[t] + sign * step_q, &cache[2 * v], &cache[2 * v + 1]);
+            cvalid[v] = 1;
+          }
+          if (!chain_mats(t, cache[2 * v], cache[2 * v + 1], m, base, ta, tb, tm, Mcur, sccur,
+                          Mvar + mvar_off(v, t, m)))
+            S[S_ERR] = 1.0;
+        }
+      }
+      mvar_valid = true;
+      __syncwarp();
+      if (S[S_ERR] != 0.0) {
+        failed = true;
+        break;
+      }
+      // neighbour groups: rigid first, then torsion neighbours in order
+      double bv = S[S_GEO];
+      int bj = -1;
+      int tg = 0;  // next torsion to schedule
+      for (int grp = 0; grp == 0 || tg < m; ++grp) {
+        int j0, jn, tlo = 0, thi = 0, items;
+        if (grp == 0) {
+          j0 = 0;
+          jn = 12;
+          items = 12 * n;
+        } else {
+          tlo = tg;
+          thi = min(m, tlo + kGroup / 2);
+          tg = thi;
+          j0 = 12 + 2 * tlo;
+          jn = 2 * (thi - tlo);
+          items = 2 * (doff[thi - 1] + dcnt[thi - 1] - doff[tlo]);
+        }
+        for (int it = lane; it < items; it += 32) {
+          bool out;
+          if (grp == 0) {
+            const int j = it / n, h = it - j * n;
+            const int a = hl[h];
+            const double *X = Rj + 16 * j;
+            vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(X, X + 9, ld3(tors + 3 * a), a), out);
+          } else {
+            const int kk = it + 2 * doff[tlo];
+            int t = tlo;
+            while (kk >= 2 * (doff[t] + dcnt[t])) ++t;
+            const int rem = kk - 2 * doff[t];
+            const int s = rem >= dcnt[t] ? 1 : 0;
+            const int h = ditems[doff[t] + rem - s * dcnt[t]];
+            const int v = 2 * t + s;
+            const int a = hl[h];
+            d3 x = ld3(base + 3 * a);
+            const uint32_t mask = tm[a];
+            for (int u = 0; u < m; ++u) {
+              if (!((mask >> u) & 1u)) continue;
+              x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
+            }
+            vb[(v - 2 * tlo) * nmax + h] =
+                field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, x, a), out);
+          }
+        }
+        __syncwarp();
+        // geo_score of each neighbour in the group (grid.cpp:97-101)
+        if (lane < jn) {
+          const double *row = vb + lane * nmax;
+          double acc = 0.0;
+          if (grp == 0) {
+            for (int h = 0; h < n; ++h) acc += row[h];
+          } else {
+            const int t = tlo + (lane >> 1);
+            for (int h = 0; h < n; ++h) acc += ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
+          }
+          scores[lane] = acc;
+        }
+        __syncwarp();
+        // first strict maximum of the group, then against the running best
+        double gv = lane < jn ? scores[lane] : -__longlong_as_double(0x7ff0000000000000LL);
+        int gj = lane < jn ? lane : 0x7fffffff;
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, gv, off);
+          const int oj = __shfl_xor_sync(0xffffffffu, gj, off);
+          if (ov > gv || (ov == gv && oj < gj)) {
+            gv = ov;
+            gj = oj;
+          }
+        }
+        if (gv > bv) {  // search.cpp:138: strictly better than everything before
+          bv = gv;
+          bj = j0 + gj;
+          const double *row = vb + gj * nmax;
+          if (grp == 0) {
+            for (int h = lane; h < n; h += 32) vbest[h] = row[h];
+          } else {
+            const int t = tlo + (gj >> 1);
+            for (int h = lane; h < n; h += 32) vbest[h] = ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
+          }
+        }
+        __syncwarp();
+      }
+      evals += (unsigned long long)n * J;
+      ++n_iter;
+      if (bj >= 0) {
+        ++n_adopt;
+        moved = true;
+        if (bj < 12) {
+          const double *X = Rj + 16 * bj;
+          if (lane < 9) S[S_R + lane] = X[lane];
+          else if (lane < 12) S[S_T + lane - 9] = X[lane];
+          else if (lane < 16) S[S_Q + lane - 12] = X[lane];
+        } else {
+          const int v = bj - 12, t = v >> 1;
+          const double sign = (v & 1) ? -1.0 : 1.0;
+          for (int i = lane; i < 12 * (m - t); i += 32) Mcur[12 * t + i] = Mvar[mvar_off(v, t, m) + i];
+          if (lane == 0) {
+            ang[t] = ang[t] + sign * step_q;
+            sccur[2 * t] = cache[2 * v];
+            sccur[2 * t + 1] = cache[2 * v + 1];
+          }
+          if (lane < 2) cvalid[2 * t + lane] = 0;
+          mvar_valid = false;
+          __syncwarp();
+          for (int a = lane; a < N; a += 32) {
+            d3 x = ld3(base + 3 * a);
+            const uint32_t mask = tm[a];
+            for (int u = 0; u < m; ++u)
+              if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
+            st3(tors + 3 * a, x);
+          }
+        }
+        for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
+        if (lane == 0) S[S_GEO] = bv;
+        __syncwarp();
+        // new pivot = centroid of the adopted conformation
+        if (lane < 3) {
+          const int row = lane;
+          auto val = [&](int a) -> double { return rigid_row(S + S_R, S + S_T, ld3(tors + 3 * a), a, row); };
+          double p = val(0);
+          if (row < 2) {
+            const int size4 = (N - 1) & ~3;
+            int i = 1;
+            for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
+            for (; i < N; ++i) p = p + val(i);
+          } else {
+            for (int i = 1; i < N; ++i) p = p + val(i);
+          }
+          S[S_PIV + row] = p / (double)N;
+        }
+      } else {
+        if (lane == 0) {
+          S[S_STEPT] = S[S_STEPT] * 0.5;
+          S[S_STEPR] = S[S_STEPR] * 0.5;
+          S[S_STEPQ] = S[S_STEPQ] * 0.5;
+        }
+        for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
+        mvar_valid = false;
+        ++level;
+      }
+      __syncwarp();
+    }
+    if (failed) {
+      if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
+      continue;
+    }
+    // ---- outputs: the pose's conformation = apply_rigid(tors, T); in
+    // local_search mode an unmoved pose returns its input conformation.
+    const size_t ck = 3 * ((size_t)a0 * k + (size_t)r * N);
+    if (ls_mode && !moved) {
+      for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
+    } else {
+      for (int a = lane; a < N; a += 32)
+        st3(A.o.conf + ck + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
+    }
+    const size_t tk = (size_t)t0 * k + (size_t)r * m;
+    for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = ang[u];
+    if (lane < 4)
+      A.o.T[7 * (size_t)item + lane] = S[S_Q + lane];
+    else if (lane < 7)
+      A.o.T[7 * (size_t)item + lane] = S[S_T + lane - 4];
+    if (lane == 0) {
+      A.o.geo[item] = S[S_GEO];
+      A.o.evals[item] = evals;
+      A.o.status[item] = VS_LIG_OK;
+      if (A.o.iters) A.o.iters[item] = n_iter;
+      if (A.o.adopts) A.o.adopts[item] = n_adopt;
+    }
+    __syncwarp();
+  }
+}
+
+namespace {
+
+cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
+  const int Nm = A.Nmax, nm = A.nmax, mm = A.mmax;
+  int o = 0;
+  auto take = [&](int n) {
+    const int at = o;
+    o += (n + 1) & ~1;  // keep 16-byte alignment
+    return at;
+  };
+  A.o_tors = take(3 * Nm);
+  A.o_Mcur = take(12 * mm);
+  A.o_Mvar = take(12 * mm * (mm + 1));
+  A.o_Rj = take(16 * 12);
+  A.o_vb = take(kGroup * nm);
+  A.o_vbest = take(nm);
+  A.o_vcur = take(nm);
+  A.o_scores = take(kGroup);
+  A.o_cache = take(4 * mm);
+  A.o_ang = take(mm);
+  A.o_sccur = take(2 * mm);
+  A.o_state = take(S_N);
+  A.o_ints = take((nm + Nm + 2 * mm + 3) / 2 + 1);
+  A.warp_doubles = o;
+  const size_t smem = (size_t)(16 + o * kWarps) * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const void *fn = A.pg.mode == 1 ? (const void *)k_search<1>
+                                  : (A.pg.mode == 2 ? (const void *)k_search<2> : (const void *)k_search<0>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarps, smem);
+  if (per_sm < 1) per_sm = 1;
+  int blocks = num_sms * per_sm;
+  const int need = (A.n_items + kWarps - 1) / kWarps;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (A.pg.mode == 1)
+    k_search<1><<<blocks, 32 * kWarps, smem, s>>>(A);
+  else if (A.pg.mode == 2)
+    k_search<2><<<blocks, 32 * kWarps, smem, s>>>(A);
+  else
+    k_search<0><<<blocks, 32 * kWarps, smem, s>>>(A);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+void set_lattice_table_search(const double *sc72) { cudaMemcpyToSymbol(c_lattice_sc_s, sc72, sizeof(double) * 72); }
+
+cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
+                          const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
+                          int num_sms, cudaStream_t s, int *launches) {
+  search_args A{};
+  A.b = b;
+  A.p = p;
+  A.pg = p.packed;
+  A.c = c;
+  A.f = f;
+  A.o = o;
+  A.work = work_counter;
+  A.n_items = b.n_lig * c.k;
+  A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
+  A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
+  A.mmax = mmax > 0 ? mmax : 1;
+  if (A.n_items == 0) return cudaSuccess;
+  return run_search(A, num_sms, s, launches);
+}
+
+cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,
+                                const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,
+                                int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s) {
+  search_args A{};
+  A.b = b;
+  A.p = p;
+  A.pg = p.packed;
+  A.c = c;
+  A.o = o;
+  A.pose_in = pose_in;
+  A.ang_in = ang_in;
+  A.conf_in = conf_in;
+  A.work = work_counter;
+  A.n_items = b.n_lig;
+  A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
+  A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
+  A.mmax = mmax > 0 ? mmax : 1;
+  if (A.n_items == 0) return cudaSuccess;
+  return run_search(A, num_sms, s, nullptr);
+}
+
+}  // namespace vsd

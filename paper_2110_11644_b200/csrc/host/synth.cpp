@@ -97,13 +97,13 @@ std::string with_digit(const char *tmpl, int digit, const char *subst) {
   return out;
 }
 
-std::string candidate(Xoshiro &rng) {
+std::string candidate(Xoshiro &rng, int rmin, int rmax) {
   std::string s;
   if (rng.below(3) == 0) s += kTails[rng.below(static_cast<int>(sizeof(kTails) / sizeof(*kTails)))];
-  const int rings = 2 + rng.below(2);
+  const int rings = rmin + rng.below(rmax - rmin + 1);
   for (int r = 0; r < rings; ++r) {
     const RingUnit &u = kRings[rng.below(static_cast<int>(sizeof(kRings) / sizeof(*kRings)))];
-    const int digit = 1 + 2 * r;  // units use digits (2r+1, 2r+2)
+    const int digit = 1;  // each unit closes its rings before the next opens: digits 1, 2 are reused
     const bool last = r + 1 == rings;
     const bool tail_after = last && rng.below(3) == 0;
     if (last && !tail_after) {
@@ -136,6 +136,9 @@ extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, 
     for (int bi = next++; bi < nblocks; bi = next++) {
       Xoshiro rng(seed * 0x9e3779b97f4a7c15ULL + static_cast<uint64_t>(bi) + 1);
       const int want = std::min(kBlock, n - bi * kBlock);
+      // ring units scale with the requested size (2-3 for ~30 heavy atoms)
+      const int rmin = std::max(1, min_heavy / 13);
+      const int rmax = std::max(rmin + 1, max_heavy / 11);
       auto &out = blocks[static_cast<size_t>(bi)];
       int64_t tries = 0;
       while (static_cast<int>(out.size()) < want) {
@@ -143,7 +146,7 @@ extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, 
           unreachable = true;
           return;
         }
-        std::string s = candidate(rng);
+        std::string s = candidate(rng, rmin, rmax);
         int heavy = 0, rot = 0;
         if (!vsprep_internal::counts(s, &heavy, &rot)) continue;
         if (heavy < min_heavy || heavy > max_heavy || rot < min_rot || rot > max_rot) continue;
