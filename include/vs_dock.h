@@ -206,6 +206,19 @@ vs_status vs_chem_score_batch(vs_context *ctx, const vs_pocket *pocket, const vs
  * status_out: n_ligands (may be NULL). */
 vs_status vs_flatten_batch(vs_context *ctx, const vs_ligand_batch *batch, int32_t max_sweeps,
                            double *conformation_out, double *angles_out, int32_t *status_out);
+/* initial_poses (search.cpp:84-107) of ONE ligand (batch->n_ligands == 1)
+ * from its stored (base) coordinates and the given flat angles: k poses
+ * (poses_out[k]) and conformations (conformations_out[k * 3 * n_atoms]);
+ * evals receives k * n_heavy. */
+vs_status vs_initial_poses(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                           const double *flat_angles, int32_t k, vs_pose *poses_out, double *conformations_out,
+                           uint64_t *evals, int32_t *status_out);
+/* cluster_and_select (search.cpp:195-236) of n_poses poses of ONE ligand
+ * (geo scores + conformations n_poses * 3 * n_atoms): writes the selected
+ * pose indices in output order (leaders, then followers) and their count. */
+vs_status vs_cluster_select(vs_context *ctx, const vs_ligand_batch *batch, int32_t n_poses, const double *geo,
+                            const double *conformations, double threshold, int32_t top, int32_t *order_out,
+                            int32_t *count_out);
 /* local_search (search.cpp:109-193) of one pose per ligand.  poses,
  * angles (n_torsions_total) and conformation (3*n_atoms_total) are read as
  * the start pose and overwritten with the result; evals (may be NULL)

@@ -39,6 +39,14 @@ vs_status vs_ligand_set_view(const vs_ligand_set *set, vs_ligand_batch *view, co
 const char *vs_ligand_set_error(const vs_ligand_set *set, int32_t i);
 void vs_ligand_set_free(vs_ligand_set *set);
 
+/* Graph analysis of ligand i of a batch (host): detect_torsions
+ * (ligand.cpp:126-139) writes the rotatable bond indices (ascending) to
+ * bonds_out (capacity n_bonds) and one right-set membership byte per atom per
+ * torsion to right_mask_out (n_torsions * n_atoms); returns the torsion
+ * count.  vs_bridge_bonds (ligand.cpp:57-99) writes one flag per bond. */
+int32_t vs_detect_torsions(const vs_ligand_batch *b, int32_t i, uint16_t *bonds_out, uint8_t *right_mask_out);
+int32_t vs_bridge_bonds(const vs_ligand_batch *b, int32_t i, uint8_t *bridge_out);
+
 /* Deterministic synthetic drug-like SMILES: candidates are assembled from
  * ring/linker/substituent fragments with a seeded xoshiro256** stream and
  * kept when the prepared graph has heavy atoms in [min_heavy, max_heavy]

@@ -317,6 +317,45 @@ def local_search(pocket, ligands, poses: np.ndarray, angles: np.ndarray, conform
     return poses, ang[:b.n_torsions_total], conf, ev[:b.n_ligands], st[:b.n_ligands]
 
 
+def initial_poses(pocket, ligand: Ligand, flat_angles, k: int, ctx: Context | None = None):
+    """initial_poses (search.cpp:84-107) from the ligand's coordinates and the
+    given flat angles.  Returns (POSE_DTYPE[k], conformations (k, N, 3), evals)."""
+    ctx = ctx or default_context()
+    dp = _dev_pocket(pocket, ctx)
+    b = _batch([ligand])
+    fa = np.ascontiguousarray(flat_angles, dtype=np.float64)
+    if fa.size == 0:
+        fa = np.zeros(1)
+    poses = np.zeros(max(k, 1), dtype=abi.POSE_DTYPE)
+    confs = np.zeros((max(k, 1) * max(ligand.n_atoms, 1), 3))
+    ev = np.zeros(1, dtype=np.uint64)
+    st = np.zeros(1, dtype=np.int32)
+    native.check(native.lib().vs_initial_poses(ctx.handle, dp.handle, C.byref(b.desc()), abi.ptr(fa, C.c_double), k,
+                                               poses.ctypes.data_as(C.POINTER(abi.PoseDesc)),
+                                               abi.ptr(confs, C.c_double), abi.ptr(ev, C.c_uint64),
+                                               abi.ptr(st, C.c_int32)), "vs_initial_poses")
+    if st[0] != abi.VS_LIG_OK:
+        raise ValueError(abi.LIGAND_STATUS_NAMES.get(int(st[0]), st[0]))
+    return poses[:k], confs[:k * ligand.n_atoms].reshape(k, ligand.n_atoms, 3), int(ev[0])
+
+
+def cluster_and_select(ligand: Ligand, geo, conformations, threshold: float, top: int,
+                       ctx: Context | None = None) -> np.ndarray:
+    """cluster_and_select (search.cpp:195-236): indices of the selected poses."""
+    ctx = ctx or default_context()
+    b = _batch([ligand])
+    geo = np.ascontiguousarray(geo, dtype=np.float64)
+    confs = np.ascontiguousarray(conformations, dtype=np.float64)
+    n = int(geo.shape[0])
+    order = np.zeros(max(n, 1), dtype=np.int32)
+    cnt = np.zeros(1, dtype=np.int32)
+    native.check(native.lib().vs_cluster_select(ctx.handle, C.byref(b.desc()), n, abi.ptr(geo, C.c_double),
+                                                abi.ptr(confs if confs.size else np.zeros(1), C.c_double), threshold,
+                                                top, abi.ptr(order, C.c_int32), abi.ptr(cnt, C.c_int32)),
+                 "vs_cluster_select")
+    return order[:int(cnt[0])]
+
+
 @dataclass
 class BatchResult:
     results: np.ndarray          # DOCK_RESULT_DTYPE per ligand

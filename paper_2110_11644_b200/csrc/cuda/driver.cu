@@ -851,6 +851,88 @@ vs_status vs_flatten_batch(vs_context *ctx, const vs_ligand_batch *batch, int32_
   return VS_OK;
 }
 
+vs_status vs_initial_poses(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                           const double *flat_angles, int32_t k, vs_pose *poses_out, double *conformations_out,
+                           uint64_t *evals, int32_t *status_out) {
+  if (!ctx || !pocket || !batch || !poses_out || !conformations_out || batch->n_ligands != 1)
+    return fail(VS_ERR_INVALID_ARGUMENT, "initial_poses takes exactly one ligand");
+  if (k < 1) return fail(VS_ERR_INVALID_ARGUMENT, "restart count must be at least 1");  // search.cpp:88
+  if (k > VS_MAX_RESTARTS) return fail(VS_ERR_LIMIT, "restarts exceed VS_MAX_RESTARTS");
+  CtxLock lock(ctx);
+  vs_scoring_config c;
+  vs_scoring_config_default(&c);
+  c.restarts = k;
+  vsd::search_cfg sc{};
+  vs_status rc;
+  if ((rc = upload_tables(ctx, c, k, sc))) return rc;
+  Staged st;
+  if ((rc = stage(ctx, batch, 0, 1, st))) return rc;
+  std::vector<double> fa(static_cast<size_t>(std::max(st.torsions, 1)), 0.0);
+  for (int t = 0; t < st.torsions; ++t) fa[static_cast<size_t>(t)] = flat_angles[t];
+  if ((rc = h2d(ctx->aux1, fa.data(), fa.size(), ctx->stream))) return rc;
+  vsd::item_out o{};
+  if ((rc = ensure_items(ctx, st, k, o))) return rc;
+  CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
+  CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(vsd::launch_initial_poses(st.b, pocket->dev(), sc, ctx->aux1.as<double>(), o, ctx->work.as<int>(), st.Nmax,
+                                     st.nmax, st.mmax, ctx->num_sms, ctx->stream));
+  std::vector<double> T(static_cast<size_t>(7) * k), geo(static_cast<size_t>(k));
+  std::vector<unsigned long long> ev(static_cast<size_t>(k));
+  std::vector<int> stat(static_cast<size_t>(k));
+  CUDA_TRY(cudaMemcpyAsync(T.data(), o.T, sizeof(double) * 7 * k, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(geo.data(), o.geo, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ev.data(), o.evals, sizeof(unsigned long long) * k, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(stat.data(), o.status, sizeof(int) * k, cudaMemcpyDeviceToHost, ctx->stream));
+  if (st.atoms)
+    CUDA_TRY(cudaMemcpyAsync(conformations_out, o.conf, sizeof(double) * 3 * st.atoms * k, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  uint64_t total = 0;
+  int status = VS_LIG_OK;
+  for (int i = 0; i < k; ++i) {
+    for (int q = 0; q < 4; ++q) poses_out[i].rotation[q] = T[7 * i + q];
+    for (int q = 0; q < 3; ++q) poses_out[i].translation[q] = T[7 * i + 4 + q];
+    poses_out[i].geo_score = geo[static_cast<size_t>(i)];
+    total += ev[static_cast<size_t>(i)];
+    if (stat[static_cast<size_t>(i)] != VS_LIG_OK) status = stat[static_cast<size_t>(i)];
+  }
+  if (evals) *evals = total;
+  if (status_out) *status_out = status;
+  return VS_OK;
+}
+
+vs_status vs_cluster_select(vs_context *ctx, const vs_ligand_batch *batch, int32_t n_poses, const double *geo,
+                            const double *conformations, double threshold, int32_t top, int32_t *order_out,
+                            int32_t *count_out) {
+  if (!ctx || !batch || !geo || !conformations || !order_out || !count_out || batch->n_ligands != 1)
+    return fail(VS_ERR_INVALID_ARGUMENT, "cluster_select takes exactly one ligand");
+  if (n_poses < 1) return fail(VS_ERR_INVALID_ARGUMENT, "cannot cluster an empty pose list");  // search.cpp:198
+  if (n_poses > 12 * 1024) return fail(VS_ERR_LIMIT, "too many poses for one cluster_select call");
+  CtxLock lock(ctx);
+  Staged st;
+  vs_status rc;
+  if ((rc = stage(ctx, batch, 0, 1, st))) return rc;
+  if ((rc = h2d(ctx->aux0, geo, static_cast<size_t>(n_poses), ctx->stream))) return rc;
+  if ((rc = h2d(ctx->aux1, conformations, 3 * static_cast<size_t>(st.atoms) * n_poses, ctx->stream))) return rc;
+  CUDA_TRY(ctx->aux2.ensure(sizeof(int) * (static_cast<size_t>(n_poses) + 1)));
+  CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  std::vector<vsd::lig_meta> meta(1);
+  CUDA_TRY(cudaMemcpyAsync(meta.data(), st.b.meta, sizeof(vsd::lig_meta), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (meta[0].status != VS_LIG_OK && meta[0].status != VS_LIG_NO_HEAVY)
+    return fail(VS_ERR_INVALID_ARGUMENT, "ligand rejected by the device checks");
+  if (meta[0].n_heavy == 0 && n_poses > 1) return fail(VS_ERR_INVALID_ARGUMENT, "no heavy atoms");
+  int *dev_out = ctx->aux2.as<int>();
+  CUDA_TRY(vsd::launch_cluster(st.b, n_poses, ctx->aux0.as<double>(), ctx->aux1.as<double>(), threshold, top, dev_out,
+                               dev_out + n_poses, ctx->stream));
+  std::vector<int> out(static_cast<size_t>(n_poses) + 1);
+  CUDA_TRY(cudaMemcpyAsync(out.data(), dev_out, sizeof(int) * (n_poses + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *count_out = out[static_cast<size_t>(n_poses)];
+  for (int i = 0; i < *count_out; ++i) order_out[i] = out[static_cast<size_t>(i)];
+  return VS_OK;
+}
+
 vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
                                 const vs_scoring_config *cfg, vs_pose *poses, double *angles, double *conformation,
                                 uint64_t *evals, int32_t *status_out) {

@@ -524,6 +524,63 @@ cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_
   return cudaGetLastError();
 }
 
+// cluster_and_select (search.cpp:195-236) of np given poses of ligand 0:
+// one CTA, the same greedy leader rule as k_select.
+__global__ void __launch_bounds__(kSelThreads) k_cluster(batch_dev b, int np, const double *geo, const double *confs,
+                                                         double threshold, int top, int *order_out, int *count_out) {
+  extern __shared__ int ci[];
+  int *order = ci, *leaders = ci + np, *followers = ci + 2 * np;
+  __shared__ int n_lead, n_follow, joined;
+  const int tid = threadIdx.x;
+  const lig_meta meta = b.meta[0];
+  const int N = meta.n_atoms, n = meta.n_heavy;
+  const uint16_t *hl = b.heavy_list;
+  if (tid == 0) {
+    n_lead = 0;
+    n_follow = 0;
+  }
+  for (int i = tid; i < np; i += blockDim.x) {
+    const double gi = geo[i];
+    int rank = 0;
+    for (int j = 0; j < np; ++j) rank += (geo[j] > gi || (geo[j] == gi && j < i)) ? 1 : 0;
+    order[rank] = i;
+  }
+  __syncthreads();
+  for (int vi = 0; vi < np; ++vi) {
+    const int idx = order[vi];
+    if (tid == 0) joined = 0;
+    __syncthreads();
+    const int nl = n_lead;
+    for (int li = tid; li < nl; li += blockDim.x) {
+      double sum = 0.0;
+      for (int h = 0; h < n; ++h) {
+        const int a = hl[h];
+        sum += sqn3(sub3(ld3(confs + 3 * ((size_t)idx * N + a)), ld3(confs + 3 * ((size_t)leaders[li] * N + a))));
+      }
+      if (sqrt(sum / (double)n) <= threshold) joined = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (joined)
+        followers[n_follow++] = idx;
+      else
+        leaders[n_lead++] = idx;
+    }
+    __syncthreads();
+  }
+  const int cnt = top < np ? top : np;
+  for (int s = tid; s < cnt; s += blockDim.x) order_out[s] = s < n_lead ? leaders[s] : followers[s - n_lead];
+  if (tid == 0) *count_out = cnt;
+}
+
+cudaError_t launch_cluster(const batch_dev &b, int np, const double *geo, const double *confs, double threshold,
+                           int top, int *order_out, int *count_out, cudaStream_t s) {
+  const size_t smem = sizeof(int) * 3 * (size_t)np;
+  cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cluster<<<1, kSelThreads, smem, s>>>(b, np, geo, confs, threshold, top, order_out, count_out);
+  return cudaGetLastError();
+}
+
 // ============================================================== sub-APIs
 __global__ void k_field(pocket_dev p, int64_t n, const double *xyz, double *out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

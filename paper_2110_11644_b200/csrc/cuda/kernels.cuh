@@ -122,6 +122,13 @@ cudaError_t launch_chem_score(const batch_dev &b, const pocket_dev &p, const dou
 cudaError_t launch_build_pocket(const double *hxyz, int nh, double cx, double cy, double cz, double radius,
                                 double ox, double oy, double oz, double h, int d0, int d1, int d2, double *values,
                                 cudaStream_t s);
+// initial_poses of each ligand from given (flat) angles: k items per ligand.
+cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *angles,
+                                 const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
+                                 int num_sms, cudaStream_t s);
+// cluster_and_select of np poses of ligand 0 (search.cpp:195-236).
+cudaError_t launch_cluster(const batch_dev &b, int np, const double *geo, const double *confs, double threshold,
+                           int top, int *order_out, int *count_out, cudaStream_t s);
 // local_search of one supplied pose per ligand (item = ligand, k = 1).
 cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,
                                 const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,

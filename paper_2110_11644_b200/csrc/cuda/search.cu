@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
       dm[h] = b.heavy_dmask[a0 + h];
     }
     for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
-    if (ls_mode) {
+    if (A.ang_in) {  // local_search / initial_poses entry points: arbitrary angles
       for (int u = lane; u < m; u += 32) {
         ang[u] = A.ang_in[t0 + u];
         sincos_cr_dev(ang[u], &sccur[2 * u], &sccur[2 * u + 1]);
@@ -213,6 +213,13 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
       st3(tors + 3 * a, x);
     }
+    // initial_poses entry point: the flat centroid of these angles
+    // (search.cpp:89-90) instead of flatten's
+    if (!ls_mode && A.ang_in) {
+      __syncwarp();
+      if (lane < 3) S[S_PIV + lane] = centroid_row(tors, N, lane);
+      __syncwarp();
+    }
     // ---- start pose: initial_poses (search.cpp:95-103) or the given one
     if (lane == 0) {
       quat q;
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
       } else {
         const double *fq = A.c.fibq + 4 * r;
         q = {fq[0], fq[1], fq[2], fq[3]};
-        const d3 rc = quat_rotate(q, ld3(A.f.centroid + 3 * l));
+        const d3 rc = quat_rotate(q, A.ang_in ? ld3(S + S_PIV) : ld3(A.f.centroid + 3 * l));
         t[0] = A.p.center[0] - rc.x;
         t[1] = A.p.center[1] - rc.y;
         t[2] = A.p.center[2] - rc.z;
@@ -573,6 +580,26 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
   A.mmax = mmax > 0 ? mmax : 1;
   if (A.n_items == 0) return cudaSuccess;
   return run_search(A, num_sms, s, launches);
+}
+
+cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *angles,
+                                 const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
+                                 int num_sms, cudaStream_t s) {
+  search_args A{};
+  A.b = b;
+  A.p = p;
+  A.pg = p.packed;
+  A.c = c;
+  A.c.max_iter = 0;  // poses only: no local_search iteration
+  A.o = o;
+  A.ang_in = angles;
+  A.work = work_counter;
+  A.n_items = b.n_lig * c.k;
+  A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
+  A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
+  A.mmax = mmax > 0 ? mmax : 1;
+  if (A.n_items == 0) return cudaSuccess;
+  return run_search(A, num_sms, s, nullptr);
 }
 
 cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,

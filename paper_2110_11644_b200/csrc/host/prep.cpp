@@ -748,4 +748,45 @@ const char *vs_ligand_set_error(const vs_ligand_set *s, int32_t i) {
 
 void vs_ligand_set_free(vs_ligand_set *s) { delete s; }
 
+static vsprep::Mol mol_of(const vs_ligand_batch *b, int32_t i) {
+  vsprep::Mol m;
+  for (int a = b->atom_offset[i]; a < b->atom_offset[i + 1]; ++a) {
+    m.elem.push_back(b->element[a]);
+    m.heavy.push_back(b->is_heavy[a] ? 1 : 0);
+    m.pos.push_back({b->xyz ? b->xyz[3 * a] : 0.0, b->xyz ? b->xyz[3 * a + 1] : 0.0, b->xyz ? b->xyz[3 * a + 2] : 0.0});
+  }
+  for (int k = b->bond_offset[i]; k < b->bond_offset[i + 1]; ++k) {
+    m.ba.push_back(b->bond_a[k]);
+    m.bb.push_back(b->bond_b[k]);
+    m.order.push_back(b->bond_order ? b->bond_order[k] : 1);
+  }
+  return m;
+}
+
+int32_t vs_detect_torsions(const vs_ligand_batch *b, int32_t i, uint16_t *bonds_out, uint8_t *right_mask_out) {
+  if (!b || i < 0 || i >= b->n_ligands) return -1;
+  vsprep::Mol m = mol_of(b, i);
+  for (std::size_t k = 0; k < m.ba.size(); ++k)
+    if (m.ba[k] >= m.n() || m.bb[k] >= m.n()) return -1;
+  vsprep::detect_torsions(m);
+  for (std::size_t t = 0; t < m.tors.size(); ++t) {
+    if (bonds_out) bonds_out[t] = m.tors[t];
+    if (right_mask_out) {
+      std::memset(right_mask_out + t * m.n(), 0, m.n());
+      for (uint16_t a : m.right[t]) right_mask_out[t * m.n() + a] = 1;
+    }
+  }
+  return static_cast<int32_t>(m.tors.size());
+}
+
+int32_t vs_bridge_bonds(const vs_ligand_batch *b, int32_t i, uint8_t *bridge_out) {
+  if (!b || i < 0 || i >= b->n_ligands) return -1;
+  vsprep::Mol m = mol_of(b, i);
+  for (std::size_t k = 0; k < m.ba.size(); ++k)
+    if (m.ba[k] >= m.n() || m.bb[k] >= m.n()) return -1;
+  const auto br = vsprep::bridge_bonds(m);
+  for (std::size_t k = 0; k < br.size(); ++k) bridge_out[k] = br[k];
+  return static_cast<int32_t>(br.size());
+}
+
 }  // extern "C"

@@ -46,6 +46,8 @@ SIGNATURES = {
     "vs_geo_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d, _u64]),
     "vs_chem_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d]),
     "vs_flatten_batch": (C.c_int, [_vp, _LB, C.c_int32, _d, _d, _i32]),
+    "vs_initial_poses": (C.c_int, [_vp, _vp, _LB, _d, C.c_int32, _PO, _d, _u64, _i32]),
+    "vs_cluster_select": (C.c_int, [_vp, _LB, C.c_int32, _d, _d, C.c_double, C.c_int32, _i32, _i32]),
     "vs_local_search_batch": (C.c_int, [_vp, _vp, _LB, _CF, _PO, _d, _d, _u64, _i32]),
     "vs_measure_peaks": (C.c_int, [C.c_int, _d]),
     # vs_prep.h
@@ -53,6 +55,8 @@ SIGNATURES = {
     "vs_ligand_set_view": (C.c_int, [_vp, _LB, C.POINTER(_i32)]),
     "vs_ligand_set_error": (C.c_char_p, [_vp, C.c_int32]),
     "vs_ligand_set_free": (None, [_vp]),
+    "vs_detect_torsions": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint8)]),
+    "vs_bridge_bonds": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint8)]),
     "vs_synth_smiles": (C.c_int64, [C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_char_p, C.c_int64]),
 }
