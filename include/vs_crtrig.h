@@ -131,10 +131,18 @@ VS_HD void sincos_cr(double x, double *s_out, double *c_out) {
   r = dd_add(r, dd{-(kd * P3t), 0.0});
   const dd r2 = dd_mul(r, r);
 
+  /* Loops kept rolled: this routine is cold on the device (called only when
+   * a torsion angle changes) and must not bloat the search kernel's code. */
   dd ps = sin_coeff(VS_SIN_TERMS - 1);
+#if defined(__CUDACC__)
+#pragma unroll 1
+#endif
   for (int n = VS_SIN_TERMS - 2; n >= 0; --n) ps = dd_add(dd_mul(ps, r2), sin_coeff(n));
   const dd sr = dd_mul(ps, r);
   dd pc = cos_coeff(VS_COS_TERMS - 1);
+#if defined(__CUDACC__)
+#pragma unroll 1
+#endif
   for (int n = VS_COS_TERMS - 2; n >= 0; --n) pc = dd_add(dd_mul(pc, r2), cos_coeff(n));
 
   /* hi parts are RN(hi + lo) after fast_two_sum normalisation. */

@@ -623,3 +623,63 @@ Pose exhaustive_dock(const Pocket &pocket, const Ligand &ligand) {
 }
 
 }  // namespace vscreen
+
+// ------------------------------------------------------------ b200 extras
+#include "vscreen/b200/prepare.hpp"
+
+namespace vscreen::b200 {
+
+static std::vector<Ligand> prep_many(const std::vector<std::string> &smiles, int mode) {
+  std::vector<const char *> ptrs;
+  for (const auto &s : smiles) ptrs.push_back(s.c_str());
+  vs_ligand_set *set = nullptr;
+  if (vs_prep_smiles_batch(static_cast<int32_t>(ptrs.size()), ptrs.data(), mode, 8, &set) != VS_OK)
+    throw InvalidArgument("vs_prep_smiles_batch failed");
+  vs_ligand_batch v{};
+  const int32_t *st = nullptr;
+  vs_ligand_set_view(set, &v, &st);
+  std::vector<Ligand> out;
+  std::string err;
+  for (std::size_t i = 0; i < smiles.size(); ++i) {
+    if (st[i] != 0) {
+      err = vs_ligand_set_error(set, static_cast<int32_t>(i));
+      break;
+    }
+    Ligand l;
+    l.name = smiles[i];
+    for (int a = v.atom_offset[i]; a < v.atom_offset[i + 1]; ++a) {
+      Atom at;
+      at.element = static_cast<Element>(v.element[a]);
+      at.is_heavy = v.is_heavy[a] != 0;
+      at.position = Eigen::Vector3d(v.xyz[3 * a], v.xyz[3 * a + 1], v.xyz[3 * a + 2]);
+      l.atoms.push_back(at);
+    }
+    for (int k = v.bond_offset[i]; k < v.bond_offset[i + 1]; ++k)
+      l.bonds.push_back({v.bond_a[k], v.bond_b[k], static_cast<BondOrder>(v.bond_order[k])});
+    for (int t = v.torsion_offset[i]; t < v.torsion_offset[i + 1]; ++t)
+      l.torsions.push_back(torsion_partition(l, v.torsion_bond[t]));
+    out.push_back(std::move(l));
+  }
+  vs_ligand_set_free(set);
+  if (!err.empty()) throw ParseError(err);
+  return out;
+}
+
+Ligand prepare_smiles(const std::string &smiles, int mode) { return prep_many({smiles}, mode)[0]; }
+
+std::vector<Ligand> prepare_ligands(const std::vector<std::string> &smiles, bool quantize) {
+  std::vector<Ligand> ligs = prep_many(smiles, 1);
+  for (Ligand &l : ligs) {
+    FlattenResult f = flatten(l, conformation_of(l), 20);
+    l = with_conformation(std::move(l), f.conformation);
+    if (quantize)
+      for (Atom &a : l.atoms)
+        for (int k = 0; k < 3; ++k) {
+          volatile float narrowed = static_cast<float>(a.position[k]);
+          a.position[k] = static_cast<double>(narrowed);
+        }
+  }
+  return ligs;
+}
+
+}  // namespace vscreen::b200

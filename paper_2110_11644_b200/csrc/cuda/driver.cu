@@ -81,7 +81,7 @@ struct vs_context {
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
   DevBuf results, best_ang, best_conf, counters, spin, fibq;
-  DevBuf aux0, aux1, aux2, aux3;
+  DevBuf aux0, aux1, aux2, aux3, search_args;
 };
 
 struct vs_pocket {
@@ -742,8 +742,9 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(cudaEventRecord(ctx->evs[1], ctx->stream));
     CUDA_TRY(vsd::launch_flatten(st.b, cfg->flatten_max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
+    CUDA_TRY(ctx->search_args.ensure(vsd::search_args_bytes()));
     CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax, ctx->num_sms,
-                                ctx->stream, nullptr));
+                                ctx->stream, nullptr, ctx->search_args.p));
     CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
     CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));
@@ -874,8 +875,9 @@ vs_status vs_initial_poses(vs_context *ctx, const vs_pocket *pocket, const vs_li
   if ((rc = ensure_items(ctx, st, k, o))) return rc;
   CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
   CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(ctx->search_args.ensure(vsd::search_args_bytes()));
   CUDA_TRY(vsd::launch_initial_poses(st.b, pocket->dev(), sc, ctx->aux1.as<double>(), o, ctx->work.as<int>(), st.Nmax,
-                                     st.nmax, st.mmax, ctx->num_sms, ctx->stream));
+                                     st.nmax, st.mmax, ctx->num_sms, ctx->stream, ctx->search_args.p));
   std::vector<double> T(static_cast<size_t>(7) * k), geo(static_cast<size_t>(k));
   std::vector<unsigned long long> ev(static_cast<size_t>(k));
   std::vector<int> stat(static_cast<size_t>(k));
@@ -958,9 +960,10 @@ vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const 
   if ((rc = ensure_items(ctx, st, 1, o))) return rc;
   CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
   CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
+  CUDA_TRY(ctx->search_args.ensure(vsd::search_args_bytes()));
   CUDA_TRY(vsd::launch_local_search(st.b, pocket->dev(), sc, ctx->aux0.as<double>(), ctx->aux1.as<double>(),
                                     ctx->aux2.as<double>(), o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax,
-                                    ctx->num_sms, ctx->stream));
+                                    ctx->num_sms, ctx->stream, ctx->search_args.p));
   std::vector<double> T(static_cast<size_t>(7) * std::max(st.n, 1)), geo(static_cast<size_t>(std::max(st.n, 1)));
   std::vector<unsigned long long> ev(static_cast<size_t>(std::max(st.n, 1)));
   std::vector<int> stat(static_cast<size_t>(std::max(st.n, 1)));

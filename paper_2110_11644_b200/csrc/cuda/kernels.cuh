@@ -110,7 +110,9 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
                            cudaStream_t s);
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
-                          int num_sms, cudaStream_t s, int *launches);
+                          int num_sms, cudaStream_t s, int *launches, void *args_buf);
+// device buffer size the search launchers need for their argument block
+size_t search_args_bytes();
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s);
 // sub-API kernels
@@ -125,13 +127,14 @@ cudaError_t launch_build_pocket(const double *hxyz, int nh, double cx, double cy
 // initial_poses of each ligand from given (flat) angles: k items per ligand.
 cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *angles,
                                  const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
-                                 int num_sms, cudaStream_t s);
+                                 int num_sms, cudaStream_t s, void *args_buf);
 // cluster_and_select of np poses of ligand 0 (search.cpp:195-236).
 cudaError_t launch_cluster(const batch_dev &b, int np, const double *geo, const double *confs, double threshold,
                            int top, int *order_out, int *count_out, cudaStream_t s);
 // local_search of one supplied pose per ligand (item = ligand, k = 1).
 cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,
                                 const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,
-                                int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s);
+                                int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s,
+                                void *args_buf);
 
 }  // namespace vsd

@@ -331,3 +331,12 @@ def test_full_size_properties(env):
     S = r1.results["scoring_evals"].astype(np.int64)
     # S = n * (k + sum_iters (12 + 2m)): the sweep count is an integer
     assert np.all((S - 30 * n) % (n * (12 + 2 * m)) == 0)
+
+
+def test_cpp_dropin_program(gpu_ctx):
+    """C++ written against the reference's API (include/vscreen) runs on the B200 build."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_build", "test_dropin")
+    assert os.path.exists(exe), "build() compiles tests/cpp/test_dropin.cpp"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
