@@ -92,6 +92,7 @@ struct vs_pocket {
   int n_protein = 0;
   DevBuf values, pxyz, pclass, cell_start, cell_atoms, packed, palette;
   int packed_mode = 0;
+  int bricks[2] = {0, 0};
   double cmin[3] = {0, 0, 0};
   double cs = 2.0;
   int cdims[3] = {0, 0, 0};
@@ -123,8 +124,8 @@ struct vs_pocket {
     p.cell_start = has_cells ? cell_start.as<int>() : nullptr;
     p.cell_atoms = has_cells ? cell_atoms.as<int>() : nullptr;
     p.packed.mode = packed_mode;
-    p.packed.cx = dims[0] - 1;
-    p.packed.cy = dims[1] - 1;
+    p.packed.cx = bricks[0];
+    p.packed.cy = bricks[1];
     p.packed.c2 = packed_mode == 1 ? packed.as<uint16_t>() : nullptr;
     p.packed.c4 = packed_mode == 2 ? packed.as<uint32_t>() : nullptr;
     p.packed.inv_h = 1.0 / spacing;  // correctly rounded reciprocal for div_h
@@ -230,7 +231,10 @@ vs_status build_packed(vs_pocket *p, const double *values) {
   CUDA_TRY(cudaMemcpy(p->palette.p, pal16.data(), sizeof(double) * 16, cudaMemcpyHostToDevice));
   if (p->packed_mode == 0) return VS_OK;
   const int cx = p->dims[0] - 1, cy = p->dims[1] - 1, cz = p->dims[2] - 1;
-  const size_t ncell = static_cast<size_t>(cx) * cy * cz;
+  const int bx = (cx + 3) / 4, by = (cy + 3) / 4, bz = (cz + 3) / 4;
+  p->bricks[0] = bx;
+  p->bricks[1] = by;
+  const size_t ncell = static_cast<size_t>(bx) * by * bz * 64;  // 4x4x4 bricks (dmath.cuh cell_index)
   const int bits = p->packed_mode == 1 ? 2 : 4;
   std::vector<uint32_t> words(ncell, 0u);
   for (int iz = 0; iz < cz; ++iz)
@@ -244,7 +248,9 @@ vs_status build_packed(vs_pocket *p, const double *values) {
                                                                  static_cast<size_t>(p->dims[1]) * (iz + dz));
           w |= static_cast<uint32_t>(code[node]) << (bits * c);
         }
-        words[static_cast<size_t>(ix) + static_cast<size_t>(cx) * (static_cast<size_t>(iy) + static_cast<size_t>(cy) * iz)] = w;
+        const size_t brick = static_cast<size_t>(ix >> 2) + static_cast<size_t>(bx) *
+                                 (static_cast<size_t>(iy >> 2) + static_cast<size_t>(by) * (iz >> 2));
+        words[(brick << 6) | ((iz & 3) << 4) | ((iy & 3) << 2) | (ix & 3)] = w;
       }
   if (p->packed_mode == 1) {
     std::vector<uint16_t> w16(ncell);

@@ -121,249 +121,8 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
   return true;
 }
 
-// Shared-memory views of one warp plus the current item's ligand tables.
-struct WarpState {
-  double *tors, *Mcur, *Mvar, *Rj, *vb, *vbest, *vcur, *scores, *cache, *ang, *sccur, *S;
-  uint32_t *dm;
-  int *cvalid;
-  int N, n, m, a0, t0, l, r, k;
-  const double *base;
-  const uint16_t *hl, *ta, *tb, *ditems;
-  const uint32_t *tm;
-  const int *dcnt, *doff;
-};
-
-// centroid_row over the conformation apply_rigid(tors, T) (or a given
-// conformation) computed on the fly: search.cpp:124 / transform.cpp:49-52.
-__device__ __noinline__ double pivot_row(const WarpState &w, const double *given, int row) {
-  const double *R = w.S + S_R, *T = w.S + S_T;
-  auto val = [&](int a) -> double {
-    if (given) return given[3 * a + row];
-    return rigid_row(R, T, ld3(w.tors + 3 * a), a, row);
-  };
-  const int N = w.N;
-  double p = val(0);
-  if (row < 2) {
-    const int size4 = (N - 1) & ~3;
-    int i = 1;
-    for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
-    for (; i < N; ++i) p = p + val(i);
-  } else {
-    for (int i = 1; i < N; ++i) p = p + val(i);
-  }
-  return p / (double)N;
-}
-
-// tors = apply_torsions(base, angles) with the current matrices (warp).
-__device__ __noinline__ void rebuild_tors(const WarpState &w, int lane) {
-  for (int a = lane; a < w.N; a += 32) {
-    d3 x = ld3(w.base + 3 * a);
-    const uint32_t mask = w.tm[a];
-    for (int u = 0; u < w.m; ++u)
-      if ((mask >> u) & 1u) x = torsion_apply(w.Mcur + 12 * u, x);
-    st3(w.tors + 3 * a, x);
-  }
-}
-
 template <int MODE>
-__device__ __noinline__ double sample_cold(const search_args &A, const double *pal, d3 p) {
-  bool out;
-  return field_value_fast<MODE>(A.p.g, A.pg, pal, p, out);
-}
-
-// Restart start-up: tables, torsion matrices, torsioned frame, start pose,
-// its samples and score, pivot.  Returns false on a degenerate axis.
-template <int MODE>
-__device__ __noinline__ bool init_restart(const search_args &A, const double *pal, WarpState &w, int lane,
-                                          unsigned long long &evals) {
-  const bool ls_mode = A.pose_in != nullptr;
-  const int m = w.m, n = w.n;
-  for (int h = lane; h < n; h += 32) w.dm[h] = A.b.heavy_dmask[w.a0 + h];
-  for (int v = lane; v < 2 * m; v += 32) w.cvalid[v] = 0;
-  if (A.ang_in) {  // local_search / initial_poses entry points: arbitrary angles
-    for (int u = lane; u < m; u += 32) {
-      w.ang[u] = A.ang_in[w.t0 + u];
-      sincos_cr_dev(w.ang[u], &w.sccur[2 * u], &w.sccur[2 * u + 1]);
-    }
-  } else {
-    for (int u = lane; u < m; u += 32) {
-      const int li = A.f.idx[w.t0 + u];
-      w.ang[u] = li * kLatticeStep;  // angles_of, search.cpp:40
-      w.sccur[2 * u] = c_lattice_sc_dev(2 * li);
-      w.sccur[2 * u + 1] = c_lattice_sc_dev(2 * li + 1);
-    }
-  }
-  if (lane == 0) w.S[S_ERR] = 0.0;
-  __syncwarp();
-  if (lane == 0 && m > 0 && !chain_mats(0, w.sccur[0], w.sccur[1], m, w.base, w.ta, w.tb, w.tm, w.Mcur, w.sccur, w.Mcur))
-    w.S[S_ERR] = 1.0;
-  __syncwarp();
-  if (w.S[S_ERR] != 0.0) return false;
-  rebuild_tors(w, lane);  // torsioned frame (search.cpp:115)
-  __syncwarp();
-  if (!ls_mode && A.ang_in) {  // initial_poses entry: flat centroid of these angles
-    if (lane < 3) w.S[S_PIV + lane] = centroid_row(w.tors, w.N, lane);
-    __syncwarp();
-  }
-  if (lane == 0) {  // start pose: initial_poses (search.cpp:95-103) or the given one
-    quat q;
-    double t[3];
-    if (ls_mode) {
-      const double *pi = A.pose_in + 8 * w.l;
-      q = {pi[0], pi[1], pi[2], pi[3]};
-      t[0] = pi[4];
-      t[1] = pi[5];
-      t[2] = pi[6];
-    } else {
-      const double *fq = A.c.fibq + 4 * w.r;
-      q = {fq[0], fq[1], fq[2], fq[3]};
-      const d3 rc = quat_rotate(q, A.ang_in ? ld3(w.S + S_PIV) : ld3(A.f.centroid + 3 * w.l));
-      t[0] = A.p.center[0] - rc.x;
-      t[1] = A.p.center[1] - rc.y;
-      t[2] = A.p.center[2] - rc.z;
-    }
-    w.S[S_Q] = q.x;
-    w.S[S_Q + 1] = q.y;
-    w.S[S_Q + 2] = q.z;
-    w.S[S_Q + 3] = q.w;
-    w.S[S_T] = t[0];
-    w.S[S_T + 1] = t[1];
-    w.S[S_T + 2] = t[2];
-    quat_matrix(q, w.S + S_R);
-    w.S[S_STEPT] = A.c.step_t;
-    w.S[S_STEPR] = A.c.step_r;
-    w.S[S_STEPQ] = A.c.step_q;
-  }
-  __syncwarp();
-  for (int h = lane; h < n; h += 32) {
-    const int a = w.hl[h];
-    w.vcur[h] = sample_cold<MODE>(A, pal, rigid_col(w.S + S_R, w.S + S_T, ld3(w.tors + 3 * a), a));
-  }
-  __syncwarp();
-  if (lane == 0) {
-    if (ls_mode) {
-      w.S[S_GEO] = A.pose_in[8 * w.l + 7];
-    } else {
-      double acc = 0.0;
-      for (int h = 0; h < n; ++h) acc += w.vcur[h];
-      w.S[S_GEO] = acc;
-    }
-  }
-  if (!ls_mode) evals += (unsigned long long)n;
-  if (lane < 3) w.S[S_PIV + lane] = pivot_row(w, ls_mode ? A.conf_in + 3 * (size_t)w.a0 : nullptr, lane);
-  __syncwarp();
-  return true;
-}
-
-// Rigid neighbour transforms (search.cpp:152-167) and, when stale, the
-// torsion-neighbour matrices (search.cpp:168-176).  Returns false on a
-// degenerate axis.
-__device__ __noinline__ bool neighbour_setup(const search_args &A, WarpState &w, int lane, int level, bool mvar_valid) {
-  const int m = w.m, J = 12 + 2 * m;
-  const double step_t = w.S[S_STEPT], step_q = w.S[S_STEPQ];
-  bool ok = true;
-  for (int j = lane; j < (mvar_valid ? 12 : J); j += 32) {
-    if (j < 12) {
-      double *X = w.Rj + 16 * j;
-      if (j < 6) {
-        const int axis = j >> 1;
-        const double sign = (j & 1) ? -1.0 : 1.0;
-        for (int q = 0; q < 9; ++q) X[q] = w.S[S_R + q];
-        for (int q = 0; q < 3; ++q) X[9 + q] = w.S[S_T + q];
-        X[9 + axis] = w.S[S_T + axis] + sign * step_t;
-        for (int q = 0; q < 4; ++q) X[12 + q] = w.S[S_Q + q];
-      } else {
-        const double *sq = A.c.spin + 4 * (6 * level + (j - 6));
-        const quat spin{sq[0], sq[1], sq[2], sq[3]};
-        const d3 piv = ld3(w.S + S_PIV);
-        const d3 spin_t = sub3(piv, quat_rotate(spin, piv));
-        const quat cur{w.S[S_Q], w.S[S_Q + 1], w.S[S_Q + 2], w.S[S_Q + 3]};
-        const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
-        const d3 tt = add3(quat_rotate(spin, ld3(w.S + S_T)), spin_t);
-        quat_matrix(qn, X);
-        X[9] = tt.x;
-        X[10] = tt.y;
-        X[11] = tt.z;
-        X[12] = qn.x;
-        X[13] = qn.y;
-        X[14] = qn.z;
-        X[15] = qn.w;
-      }
-    } else {
-      const int v = j - 12, t = v >> 1;
-      const double sign = (v & 1) ? -1.0 : 1.0;
-      if (!w.cvalid[v]) {
-        sincos_cr_dev(w.ang[t] + sign * step_q, &w.cache[2 * v], &w.cache[2 * v + 1]);
-        w.cvalid[v] = 1;
-      }
-      if (!chain_mats(t, w.cache[2 * v], w.cache[2 * v + 1], m, w.base, w.ta, w.tb, w.tm, w.Mcur, w.sccur,
-                      w.Mvar + mvar_off(v, t, m)))
-        ok = false;
-    }
-  }
-  return __all_sync(0xffffffffu, ok);
-}
-
-// Adopt neighbour bj (search.cpp:178-185) whose per-atom samples are vbest.
-__device__ __noinline__ void adopt(WarpState &w, int lane, int bj, double bv) {
-  const int m = w.m;
-  if (bj < 12) {
-    const double *X = w.Rj + 16 * bj;
-    if (lane < 9)
-      w.S[S_R + lane] = X[lane];
-    else if (lane < 12)
-      w.S[S_T + lane - 9] = X[lane];
-    else if (lane < 16)
-      w.S[S_Q + lane - 12] = X[lane];
-  } else {
-    const int v = bj - 12, t = v >> 1;
-    const double sign = (v & 1) ? -1.0 : 1.0;
-    const double step_q = w.S[S_STEPQ];
-    for (int i = lane; i < 12 * (m - t); i += 32) w.Mcur[12 * t + i] = w.Mvar[mvar_off(v, t, m) + i];
-    if (lane == 0) {
-      w.ang[t] = w.ang[t] + sign * step_q;
-      w.sccur[2 * t] = w.cache[2 * v];
-      w.sccur[2 * t + 1] = w.cache[2 * v + 1];
-    }
-    if (lane < 2) w.cvalid[2 * t + lane] = 0;
-    __syncwarp();
-    rebuild_tors(w, lane);
-  }
-  for (int h = lane; h < w.n; h += 32) w.vcur[h] = w.vbest[h];
-  if (lane == 0) w.S[S_GEO] = bv;
-  __syncwarp();
-  if (lane < 3) w.S[S_PIV + lane] = pivot_row(w, nullptr, lane);  // new pivot
-}
-
-__device__ __noinline__ void write_outputs(const search_args &A, const WarpState &w, int lane, int item, bool moved,
-                                           unsigned long long evals, int n_iter, int n_adopt) {
-  const bool ls_mode = A.pose_in != nullptr;
-  const int N = w.N, m = w.m;
-  const size_t ck = 3 * ((size_t)w.a0 * w.k + (size_t)w.r * N);
-  if (ls_mode && !moved) {  // an unmoved pose keeps its input conformation
-    for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)w.a0 + i];
-  } else {
-    for (int a = lane; a < N; a += 32)
-      st3(A.o.conf + ck + 3 * a, rigid_col(w.S + S_R, w.S + S_T, ld3(w.tors + 3 * a), a));
-  }
-  const size_t tk = (size_t)w.t0 * w.k + (size_t)w.r * m;
-  for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = w.ang[u];
-  if (lane < 4)
-    A.o.T[7 * (size_t)item + lane] = w.S[S_Q + lane];
-  else if (lane < 7)
-    A.o.T[7 * (size_t)item + lane] = w.S[S_T + lane - 4];
-  if (lane == 0) {
-    A.o.geo[item] = w.S[S_GEO];
-    A.o.evals[item] = evals;
-    A.o.status[item] = VS_LIG_OK;
-    if (A.o.iters) A.o.iters[item] = n_iter;
-    if (A.o.adopts) A.o.adopts[item] = n_adopt;
-  }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(32 * kWarps, 4) k_search(const search_args *__restrict__ Ap) {
-  const search_args &A = *Ap;  // lives in global memory: the cold paths take it by reference
+__global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
   extern __shared__ double sm[];
   double *pal = sm;  // 16 palette values (CTA-wide)
   const int lane = threadIdx.x & 31;
@@ -371,133 +130,283 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(const search_args *__
   if (threadIdx.x < 16) pal[threadIdx.x] = MODE == 0 ? 0.0 : A.p.palette[threadIdx.x];
   __syncthreads();
   double *W = sm + 16 + (size_t)warp * A.warp_doubles;
-  WarpState w;
-  w.tors = W + A.o_tors;
-  w.Mcur = W + A.o_Mcur;
-  w.Mvar = W + A.o_Mvar;
-  w.Rj = W + A.o_Rj;
-  w.vb = W + A.o_vb;
-  w.vbest = W + A.o_vbest;
-  w.vcur = W + A.o_vcur;
-  w.scores = W + A.o_scores;
-  w.cache = W + A.o_cache;
-  w.ang = W + A.o_ang;
-  w.sccur = W + A.o_sccur;
-  w.S = W + A.o_state;
-  w.dm = reinterpret_cast<uint32_t *>(W + A.o_ints);
-  w.cvalid = reinterpret_cast<int *>(w.dm + A.nmax);
-  const int k = A.pose_in ? 1 : A.c.k;
-  w.k = k;
-  const int nmax = A.nmax;
+  double *tors = W + A.o_tors;
+  double *Mcur = W + A.o_Mcur;
+  double *Mvar = W + A.o_Mvar;
+  double *Rj = W + A.o_Rj;
+  double *vb = W + A.o_vb;
+  double *vbest = W + A.o_vbest;
+  double *vcur = W + A.o_vcur;
+  double *scores = W + A.o_scores;
+  double *cache = W + A.o_cache;
+  double *ang = W + A.o_ang;
+  double *sccur = W + A.o_sccur;
+  double *S = W + A.o_state;
+  uint32_t *dm = reinterpret_cast<uint32_t *>(W + A.o_ints);
+  int *hidx = reinterpret_cast<int *>(dm + A.nmax);
+  int *cvalid = hidx + A.Nmax;
+
+  const batch_dev &b = A.b;
   const grid_view &g = A.p.g;
   const packed_grid &pg = A.pg;
+  const bool ls_mode = A.pose_in != nullptr;
+  const int k = ls_mode ? 1 : A.c.k;
+  const int nmax = A.nmax;
 
   while (true) {
     int item = 0;
     if (lane == 0) item = atomicAdd(A.work, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= A.n_items) break;
-    w.l = item / k;
-    w.r = item - w.l * k;
-    const lig_meta meta = A.b.meta[w.l];
+    const int l = item / k, r = item - l * k;
+    const lig_meta meta = b.meta[l];
     if (meta.status != VS_LIG_OK) {
       if (lane == 0) A.o.status[item] = meta.status;
       continue;
     }
-    w.N = meta.n_atoms;
-    w.n = meta.n_heavy;
-    w.m = meta.m;
-    w.a0 = A.b.atom_off[w.l];
-    w.t0 = A.b.tors_off[w.l];
-    w.base = A.b.xyz + 3 * (size_t)w.a0;
-    w.hl = A.b.heavy_list + w.a0;
-    w.tm = A.b.atom_tmask + w.a0;
-    w.ta = A.b.tors_a + w.t0;
-    w.tb = A.b.tors_b + w.t0;
-    w.dcnt = A.b.d_count + w.t0;
-    w.doff = A.b.d_off + w.t0;
-    w.ditems = A.b.ditems + A.b.ditem_base[w.l];
-    const int n = w.n, m = w.m, J = 12 + 2 * m;
+    const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
+    const int a0 = b.atom_off[l], t0 = b.tors_off[l];
+    const double *base = b.xyz + 3 * (size_t)a0;
+    const uint16_t *hl = b.heavy_list + a0;
+    const uint32_t *tm = b.atom_tmask + a0;
+    const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
+    const int *dcnt = b.d_count + t0, *doff = b.d_off + t0;
+    const uint16_t *ditems = b.ditems + b.ditem_base[l];
+    const int J = 12 + 2 * m;
     unsigned long long evals = 0;
-    if (!init_restart<MODE>(A, pal, w, lane, evals)) {
+
+    // ---- per-ligand tables
+    for (int a = lane; a < N; a += 32) hidx[a] = -1;
+    __syncwarp();
+    for (int h = lane; h < n; h += 32) {
+      hidx[hl[h]] = h;
+      dm[h] = b.heavy_dmask[a0 + h];
+    }
+    for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
+    if (A.ang_in) {  // local_search / initial_poses entry points: arbitrary angles
+      for (int u = lane; u < m; u += 32) {
+        ang[u] = A.ang_in[t0 + u];
+        sincos_cr_dev(ang[u], &sccur[2 * u], &sccur[2 * u + 1]);
+      }
+    } else {
+      for (int u = lane; u < m; u += 32) {
+        const int li = A.f.idx[t0 + u];
+        ang[u] = li * kLatticeStep;  // angles_of, search.cpp:40
+        sccur[2 * u] = c_lattice_sc_dev(2 * li);
+        sccur[2 * u + 1] = c_lattice_sc_dev(2 * li + 1);
+      }
+    }
+    if (lane == 0) S[S_ERR] = 0.0;
+    __syncwarp();
+    if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, base, ta, tb, tm, Mcur, sccur, Mcur))
+      S[S_ERR] = 1.0;
+    __syncwarp();
+    if (S[S_ERR] != 0.0) {
       if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
       continue;
     }
+    // torsioned frame (search.cpp:115)
+    for (int a = lane; a < N; a += 32) {
+      d3 x = ld3(base + 3 * a);
+      const uint32_t mask = tm[a];
+      for (int u = 0; u < m; ++u)
+        if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
+      st3(tors + 3 * a, x);
+    }
+    // initial_poses entry point: the flat centroid of these angles
+    // (search.cpp:89-90) instead of flatten's
+    if (!ls_mode && A.ang_in) {
+      __syncwarp();
+      if (lane < 3) S[S_PIV + lane] = centroid_row(tors, N, lane);
+      __syncwarp();
+    }
+    // ---- start pose: initial_poses (search.cpp:95-103) or the given one
+    if (lane == 0) {
+      quat q;
+      double t[3];
+      if (ls_mode) {
+        const double *pi = A.pose_in + 8 * l;
+        q = {pi[0], pi[1], pi[2], pi[3]};
+        t[0] = pi[4];
+        t[1] = pi[5];
+        t[2] = pi[6];
+      } else {
+        const double *fq = A.c.fibq + 4 * r;
+        q = {fq[0], fq[1], fq[2], fq[3]};
+        const d3 rc = quat_rotate(q, A.ang_in ? ld3(S + S_PIV) : ld3(A.f.centroid + 3 * l));
+        t[0] = A.p.center[0] - rc.x;
+        t[1] = A.p.center[1] - rc.y;
+        t[2] = A.p.center[2] - rc.z;
+      }
+      S[S_Q] = q.x;
+      S[S_Q + 1] = q.y;
+      S[S_Q + 2] = q.z;
+      S[S_Q + 3] = q.w;
+      S[S_T] = t[0];
+      S[S_T + 1] = t[1];
+      S[S_T + 2] = t[2];
+      quat_matrix(q, S + S_R);
+      S[S_STEPT] = A.c.step_t;
+      S[S_STEPR] = A.c.step_r;
+      S[S_STEPQ] = A.c.step_q;
+    }
+    __syncwarp();
+    for (int h = lane; h < n; h += 32) {
+      const int a = hl[h];
+      bool out;
+      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a), out);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (ls_mode) {
+        S[S_GEO] = A.pose_in[8 * l + 7];
+      } else {
+        double acc = 0.0;
+        for (int h = 0; h < n; ++h) acc += vcur[h];
+        S[S_GEO] = acc;
+      }
+    }
+    if (!ls_mode) evals += (unsigned long long)n;
+    // pivot of the start pose: centroid of its conformation (search.cpp:124)
+    if (lane < 3) {
+      const int row = lane;
+      double p;
+      auto val = [&](int a) -> double {
+        if (ls_mode) return A.conf_in[3 * ((size_t)a0 + a) + row];
+        return rigid_row(S + S_R, S + S_T, ld3(tors + 3 * a), a, row);
+      };
+      p = val(0);
+      if (row < 2) {
+        const int size4 = (N - 1) & ~3;
+        int i = 1;
+        for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
+        for (; i < N; ++i) p = p + val(i);
+      } else {
+        for (int i = 1; i < N; ++i) p = p + val(i);
+      }
+      S[S_PIV + row] = p / (double)N;
+    }
+    __syncwarp();
 
-    // register copies of the per-item views for the hot loop
-    double *const tors = w.tors, *const Mcur = w.Mcur, *const Mvar = w.Mvar, *const Rj = w.Rj, *const vb = w.vb;
-    double *const vbest = w.vbest, *const vcur = w.vcur, *const scores = w.scores, *const S = w.S;
-    const uint32_t *const dm = w.dm, *const tm = w.tm;
-    const uint16_t *const hl = w.hl, *const ditems = w.ditems;
-    const int *const dcnt = w.dcnt, *const doff = w.doff;
-    const double *const base = w.base;
     // ---- local_search (search.cpp:121-191)
     int level = 0, n_iter = 0, n_adopt = 0;
     bool failed = false, mvar_valid = false, moved = false;
     for (int iter = 0; iter < A.c.max_iter && S[S_STEPT] >= A.c.min_t; ++iter) {
-      if (!neighbour_setup(A, w, lane, level, mvar_valid)) {
-        failed = true;
-        break;
+      const double step_t = S[S_STEPT], step_q = S[S_STEPQ];
+      // rigid neighbour transforms (lanes 0-11) and, when stale, the
+      // torsion-neighbour matrices (lanes 12..; one lane per neighbour)
+      for (int w = lane; w < (mvar_valid ? 12 : J); w += 32) {
+        if (w < 12) {
+          double *X = Rj + 16 * w;
+          if (w < 6) {  // translations (search.cpp:152-158)
+            const int axis = w >> 1;
+            const double sign = (w & 1) ? -1.0 : 1.0;
+            for (int q = 0; q < 9; ++q) X[q] = S[S_R + q];
+            for (int q = 0; q < 3; ++q) X[9 + q] = S[S_T + q];
+            X[9 + axis] = S[S_T + axis] + sign * step_t;
+            for (int q = 0; q < 4; ++q) X[12 + q] = S[S_Q + q];
+          } else {  // rotations about the pivot (search.cpp:159-167)
+            const double *sq = A.c.spin + 4 * (6 * level + (w - 6));
+            const quat spin{sq[0], sq[1], sq[2], sq[3]};
+            const d3 piv = ld3(S + S_PIV);
+            const d3 spin_t = sub3(piv, quat_rotate(spin, piv));
+            const quat cur{S[S_Q], S[S_Q + 1], S[S_Q + 2], S[S_Q + 3]};
+            const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
+            const d3 tt = add3(quat_rotate(spin, ld3(S + S_T)), spin_t);
+            quat_matrix(qn, X);
+            X[9] = tt.x;
+            X[10] = tt.y;
+            X[11] = tt.z;
+            X[12] = qn.x;
+            X[13] = qn.y;
+            X[14] = qn.z;
+            X[15] = qn.w;
+          }
+        } else {  // torsion neighbour matrices (search.cpp:168-176)
+          const int v = w - 12, t = v >> 1;
+          const double sign = (v & 1) ? -1.0 : 1.0;
+          if (!cvalid[v]) {
+            sincos_cr_dev(ang[t] + sign * step_q, &cache[2 * v], &cache[2 * v + 1]);
+            cvalid[v] = 1;
+          }
+          if (!chain_mats(t, cache[2 * v], cache[2 * v + 1], m, base, ta, tb, tm, Mcur, sccur,
+                          Mvar + mvar_off(v, t, m)))
+            S[S_ERR] = 1.0;
+        }
       }
       mvar_valid = true;
       __syncwarp();
+      if (S[S_ERR] != 0.0) {
+        failed = true;
+        break;
+      }
       // neighbour groups: rigid first, then torsion neighbours in order
       double bv = S[S_GEO];
       int bj = -1;
-      int tg = 0;
+      int tg = 0;  // next torsion to schedule
       for (int grp = 0; grp == 0 || tg < m; ++grp) {
-        int j0, jn, tlo = 0, items;
+        int j0, jn, tlo = 0, thi = 0, items;
         if (grp == 0) {
           j0 = 0;
           jn = 12;
           items = 12 * n;
         } else {
           tlo = tg;
-          const int thi = min(m, tlo + kGroup / 2);
+          thi = min(m, tlo + kGroup / 2);
           tg = thi;
           j0 = 12 + 2 * tlo;
           jn = 2 * (thi - tlo);
           items = 2 * (doff[thi - 1] + dcnt[thi - 1] - doff[tlo]);
         }
-        for (int it = lane; it < items; it += 32) {
-          d3 p;
-          int row, h;
-          if (grp == 0) {
-            const int j = it / n;
-            h = it - j * n;
-            const int a = hl[h];
-            const double *X = Rj + 16 * j;
-            p = rigid_col(X, X + 9, ld3(tors + 3 * a), a);
-            row = j;
-          } else {
-            const int kk = it + 2 * doff[tlo];
-            int t = tlo;
-            while (kk >= 2 * (doff[t] + dcnt[t])) ++t;
-            const int rem = kk - 2 * doff[t];
-            const int s = rem >= dcnt[t] ? 1 : 0;
-            h = ditems[doff[t] + rem - s * dcnt[t]];
-            const int v = 2 * t + s;
-            const int a = hl[h];
-            d3 x = ld3(base + 3 * a);
-            const uint32_t mask = tm[a];
-            for (int u = 0; u < m; ++u) {
-              if (!((mask >> u) & 1u)) continue;
-              x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
+        // two items per lane per step: independent gathers in flight (ILP)
+        for (int it0 = lane; it0 < items; it0 += 64) {
+          d3 p[2];
+          int dst[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int it = min(it0 + 32 * q, items - 1);
+            if (grp == 0) {
+              const int j = it / n, h = it - j * n;
+              const int a = hl[h];
+              const double *X = Rj + 16 * j;
+              p[q] = rigid_col(X, X + 9, ld3(tors + 3 * a), a);
+              dst[q] = j * nmax + h;
+            } else {
+              const int kk = it + 2 * doff[tlo];
+              int t = tlo;
+              while (kk >= 2 * (doff[t] + dcnt[t])) ++t;
+              const int rem = kk - 2 * doff[t];
+              const int s = rem >= dcnt[t] ? 1 : 0;
+              const int h = ditems[doff[t] + rem - s * dcnt[t]];
+              const int v = 2 * t + s;
+              const int a = hl[h];
+              d3 x = ld3(base + 3 * a);
+              const uint32_t mask = tm[a];
+              for (int u = 0; u < m; ++u) {
+                if (!((mask >> u) & 1u)) continue;
+                x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
+              }
+              p[q] = rigid_col(S + S_R, S + S_T, x, a);
+              dst[q] = (v - 2 * tlo) * nmax + h;
             }
-            p = rigid_col(S + S_R, S + S_T, x, a);
-            row = v - 2 * tlo;
           }
           bool out;
-          vb[row * nmax + h] = field_value_fast<MODE>(g, pg, pal, p, out);
+          const double v0 = field_value_fast<MODE>(g, pg, pal, p[0], out);
+          const double v1 = field_value_fast<MODE>(g, pg, pal, p[1], out);
+          vb[dst[0]] = v0;
+          if (it0 + 32 < items) vb[dst[1]] = v1;
         }
         __syncwarp();
         // geo_score of each neighbour in the group (grid.cpp:97-101)
         if (lane < jn) {
-          const double *rowp = vb + lane * nmax;
+          const double *row = vb + lane * nmax;
           double acc = 0.0;
-          const int t = grp == 0 ? 31 : tlo + (lane >> 1);
-          const uint32_t bit = grp == 0 ? 0xffffffffu : (1u << t);
-          for (int h = 0; h < n; ++h) acc += (dm[h] & bit) || grp == 0 ? rowp[h] : vcur[h];
+          if (grp == 0) {
+            for (int h = 0; h < n; ++h) acc += row[h];
+          } else {
+            const int t = tlo + (lane >> 1);
+            for (int h = 0; h < n; ++h) acc += ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
+          }
           scores[lane] = acc;
         }
         __syncwarp();
@@ -515,9 +424,13 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(const search_args *__
         if (gv > bv) {  // search.cpp:138: strictly better than everything before
           bv = gv;
           bj = j0 + gj;
-          const double *rowp = vb + gj * nmax;
-          const uint32_t bit = grp == 0 ? 0xffffffffu : (1u << (tlo + (gj >> 1)));
-          for (int h = lane; h < n; h += 32) vbest[h] = (dm[h] & bit) || grp == 0 ? rowp[h] : vcur[h];
+          const double *row = vb + gj * nmax;
+          if (grp == 0) {
+            for (int h = lane; h < n; h += 32) vbest[h] = row[h];
+          } else {
+            const int t = tlo + (gj >> 1);
+            for (int h = lane; h < n; h += 32) vbest[h] = ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
+          }
         }
         __syncwarp();
       }
@@ -526,15 +439,56 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(const search_args *__
       if (bj >= 0) {
         ++n_adopt;
         moved = true;
-        if (bj >= 12) mvar_valid = false;
-        adopt(w, lane, bj, bv);
+        if (bj < 12) {
+          const double *X = Rj + 16 * bj;
+          if (lane < 9) S[S_R + lane] = X[lane];
+          else if (lane < 12) S[S_T + lane - 9] = X[lane];
+          else if (lane < 16) S[S_Q + lane - 12] = X[lane];
+        } else {
+          const int v = bj - 12, t = v >> 1;
+          const double sign = (v & 1) ? -1.0 : 1.0;
+          for (int i = lane; i < 12 * (m - t); i += 32) Mcur[12 * t + i] = Mvar[mvar_off(v, t, m) + i];
+          if (lane == 0) {
+            ang[t] = ang[t] + sign * step_q;
+            sccur[2 * t] = cache[2 * v];
+            sccur[2 * t + 1] = cache[2 * v + 1];
+          }
+          if (lane < 2) cvalid[2 * t + lane] = 0;
+          mvar_valid = false;
+          __syncwarp();
+          for (int a = lane; a < N; a += 32) {
+            d3 x = ld3(base + 3 * a);
+            const uint32_t mask = tm[a];
+            for (int u = 0; u < m; ++u)
+              if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
+            st3(tors + 3 * a, x);
+          }
+        }
+        for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
+        if (lane == 0) S[S_GEO] = bv;
+        __syncwarp();
+        // new pivot = centroid of the adopted conformation
+        if (lane < 3) {
+          const int row = lane;
+          auto val = [&](int a) -> double { return rigid_row(S + S_R, S + S_T, ld3(tors + 3 * a), a, row); };
+          double p = val(0);
+          if (row < 2) {
+            const int size4 = (N - 1) & ~3;
+            int i = 1;
+            for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
+            for (; i < N; ++i) p = p + val(i);
+          } else {
+            for (int i = 1; i < N; ++i) p = p + val(i);
+          }
+          S[S_PIV + row] = p / (double)N;
+        }
       } else {
         if (lane == 0) {
           S[S_STEPT] = S[S_STEPT] * 0.5;
           S[S_STEPR] = S[S_STEPR] * 0.5;
           S[S_STEPQ] = S[S_STEPQ] * 0.5;
         }
-        for (int v = lane; v < 2 * m; v += 32) w.cvalid[v] = 0;
+        for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
         mvar_valid = false;
         ++level;
       }
@@ -544,14 +498,35 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(const search_args *__
       if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
       continue;
     }
-    write_outputs(A, w, lane, item, moved, evals, n_iter, n_adopt);
+    // ---- outputs: the pose's conformation = apply_rigid(tors, T); in
+    // local_search mode an unmoved pose returns its input conformation.
+    const size_t ck = 3 * ((size_t)a0 * k + (size_t)r * N);
+    if (ls_mode && !moved) {
+      for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
+    } else {
+      for (int a = lane; a < N; a += 32)
+        st3(A.o.conf + ck + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
+    }
+    const size_t tk = (size_t)t0 * k + (size_t)r * m;
+    for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = ang[u];
+    if (lane < 4)
+      A.o.T[7 * (size_t)item + lane] = S[S_Q + lane];
+    else if (lane < 7)
+      A.o.T[7 * (size_t)item + lane] = S[S_T + lane - 4];
+    if (lane == 0) {
+      A.o.geo[item] = S[S_GEO];
+      A.o.evals[item] = evals;
+      A.o.status[item] = VS_LIG_OK;
+      if (A.o.iters) A.o.iters[item] = n_iter;
+      if (A.o.adopts) A.o.adopts[item] = n_adopt;
+    }
     __syncwarp();
   }
 }
 
 namespace {
 
-cudaError_t run_search(search_args &A, search_args *dev_args, int num_sms, cudaStream_t s, int *launches) {
+cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
   const int Nm = A.Nmax, nm = A.nmax, mm = A.mmax;
   int o = 0;
   auto take = [&](int n) {
@@ -571,7 +546,7 @@ cudaError_t run_search(search_args &A, search_args *dev_args, int num_sms, cudaS
   A.o_ang = take(mm);
   A.o_sccur = take(2 * mm);
   A.o_state = take(S_N);
-  A.o_ints = take((nm + 2 * mm + 3) / 2 + 1);
+  A.o_ints = take((nm + Nm + 2 * mm + 3) / 2 + 1);
   A.warp_doubles = o;
   const size_t smem = (size_t)(16 + o * kWarps) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
@@ -586,14 +561,12 @@ cudaError_t run_search(search_args &A, search_args *dev_args, int num_sms, cudaS
   const int need = (A.n_items + kWarps - 1) / kWarps;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  e = cudaMemcpyAsync(dev_args, &A, sizeof(search_args), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return e;
   if (A.pg.mode == 1)
-    k_search<1><<<blocks, 32 * kWarps, smem, s>>>(dev_args);
+    k_search<1><<<blocks, 32 * kWarps, smem, s>>>(A);
   else if (A.pg.mode == 2)
-    k_search<2><<<blocks, 32 * kWarps, smem, s>>>(dev_args);
+    k_search<2><<<blocks, 32 * kWarps, smem, s>>>(A);
   else
-    k_search<0><<<blocks, 32 * kWarps, smem, s>>>(dev_args);
+    k_search<0><<<blocks, 32 * kWarps, smem, s>>>(A);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -607,6 +580,7 @@ size_t search_args_bytes() { return sizeof(search_args); }
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf) {
+  (void)args_buf;
   search_args A{};
   A.b = b;
   A.p = p;
@@ -620,12 +594,13 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
   if (A.n_items == 0) return cudaSuccess;
-  return run_search(A, static_cast<search_args *>(args_buf), num_sms, s, launches);
+  return run_search(A, num_sms, s, launches);
 }
 
 cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *angles,
                                  const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                                  int num_sms, cudaStream_t s, void *args_buf) {
+  (void)args_buf;
   search_args A{};
   A.b = b;
   A.p = p;
@@ -640,13 +615,14 @@ cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const 
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
   if (A.n_items == 0) return cudaSuccess;
-  return run_search(A, static_cast<search_args *>(args_buf), num_sms, s, nullptr);
+  return run_search(A, num_sms, s, nullptr);
 }
 
 cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *pose_in,
                                 const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,
                                 int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s,
                                 void *args_buf) {
+  (void)args_buf;
   search_args A{};
   A.b = b;
   A.p = p;
@@ -662,7 +638,7 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
   if (A.n_items == 0) return cudaSuccess;
-  return run_search(A, static_cast<search_args *>(args_buf), num_sms, s, nullptr);
+  return run_search(A, num_sms, s, nullptr);
 }
 
 }  // namespace vsd
