@@ -76,7 +76,7 @@ struct vs_context {
   // batch inputs
   DevBuf atom_off, bond_off, tors_off, ditem_base, xyz, elem, heavy, bond_a, bond_b, tors_bond, right_off, right_atoms;
   // derived
-  DevBuf meta, tmask, heavy_list, dmask, tors_a, tors_b, d_count, d_off, ditems;
+  DevBuf meta, tmask, heavy_list, dmask, tors_a, tors_b, d_count, d_off, ditems, titems;
   // flatten / search / select
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
@@ -353,6 +353,7 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   CUDA_TRY(ctx->d_count.ensure(4 * nt));
   CUDA_TRY(ctx->d_off.ensure(4 * nt));
   CUDA_TRY(ctx->ditems.ensure(2 * static_cast<size_t>(std::max(dbase, 1))));
+  CUDA_TRY(ctx->titems.ensure(4 * static_cast<size_t>(std::max(dbase, 1))));
   vsd::batch_dev &b = st.b;
   b.n_lig = n;
   b.atom_off = ctx->atom_off.as<int>();
@@ -376,6 +377,7 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   b.d_count = ctx->d_count.as<int>();
   b.d_off = ctx->d_off.as<int>();
   b.ditems = ctx->ditems.as<uint16_t>();
+  b.titems = ctx->titems.as<uint16_t>();
   return VS_OK;
 }
 

@@ -118,6 +118,11 @@ __global__ void k_setup(batch_dev b, int restarts) {
     }
     b.d_count[t0 + t] = cnt;
     b.d_off[t0 + t] = off;
+    // the 2*cnt search items of neighbours (t,+) and (t,-), in that order
+    for (int s = 0; s < 2; ++s)
+      for (int i = 0; i < cnt; ++i)
+        b.titems[2 * base + 2 * off + s * cnt + i] =
+            (uint16_t)(((2 * t + s) << 8) | b.ditems[base + off + i]);
     off += cnt;
   }
   b.meta[l] = meta;

@@ -45,6 +45,7 @@ struct batch_dev {
   int *d_count;            // torsions: |D_t ∩ heavy|
   int *d_off;              // torsions: offset of D_t items in the ligand list
   uint16_t *ditems;        // ditem_base[l] + ...: heavy indices of D_t items
+  uint16_t *titems;        // 2*ditem_base[l] + ...: torsion-neighbour items ((2t+s) << 8) | h
 };
 
 struct pocket_dev {

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
     const uint32_t *tm = b.atom_tmask + a0;
     const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
     const int *dcnt = b.d_count + t0, *doff = b.d_off + t0;
-    const uint16_t *ditems = b.ditems + b.ditem_base[l];
+    const uint16_t *titems = b.titems + 2 * b.ditem_base[l];
     const int J = 12 + 2 * m;
     unsigned long long evals = 0;
 
@@ -358,27 +358,40 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
           jn = 2 * (thi - tlo);
           items = 2 * (doff[thi - 1] + dcnt[thi - 1] - doff[tlo]);
         }
-        // two items per lane per step: independent gathers in flight (ILP)
-        for (int it0 = lane; it0 < items; it0 += 64) {
-          d3 p[2];
-          int dst[2];
+        // Two items per lane per step (independent gathers in flight); the
+        // rigid and the torsion neighbours run in separate compact loops.
+        if (grp == 0) {
+          const float rn = 1.0f / (float)n;
+          for (int it0 = lane; it0 < items; it0 += 64) {
+            d3 p[2];
+            int dst[2];
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int it = min(it0 + 32 * q, items - 1);
-            if (grp == 0) {
-              const int j = it / n, h = it - j * n;
+            for (int q = 0; q < 2; ++q) {
+              const int it = min(it0 + 32 * q, items - 1);
+              int j = __float2int_rz((float)it * rn);
+              j -= (j * n > it) ? 1 : 0;
+              j += ((j + 1) * n <= it) ? 1 : 0;
+              const int h = it - j * n;
               const int a = hl[h];
               const double *X = Rj + 16 * j;
               p[q] = rigid_col(X, X + 9, ld3(tors + 3 * a), a);
               dst[q] = j * nmax + h;
-            } else {
-              const int kk = it + 2 * doff[tlo];
-              int t = tlo;
-              while (kk >= 2 * (doff[t] + dcnt[t])) ++t;
-              const int rem = kk - 2 * doff[t];
-              const int s = rem >= dcnt[t] ? 1 : 0;
-              const int h = ditems[doff[t] + rem - s * dcnt[t]];
-              const int v = 2 * t + s;
+            }
+            bool out;
+            const double v0 = field_value_fast<MODE>(g, pg, pal, p[0], out);
+            const double v1 = field_value_fast<MODE>(g, pg, pal, p[1], out);
+            vb[dst[0]] = v0;
+            if (it0 + 32 < items) vb[dst[1]] = v1;
+          }
+        } else {
+          const uint16_t *ti = titems + 2 * doff[tlo];
+          for (int it0 = lane; it0 < items; it0 += 64) {
+            d3 p[2];
+            int dst[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int e = ti[min(it0 + 32 * q, items - 1)];
+              const int v = e >> 8, h = e & 255, t = v >> 1;
               const int a = hl[h];
               d3 x = ld3(base + 3 * a);
               const uint32_t mask = tm[a];
@@ -389,12 +402,12 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
               p[q] = rigid_col(S + S_R, S + S_T, x, a);
               dst[q] = (v - 2 * tlo) * nmax + h;
             }
+            bool out;
+            const double v0 = field_value_fast<MODE>(g, pg, pal, p[0], out);
+            const double v1 = field_value_fast<MODE>(g, pg, pal, p[1], out);
+            vb[dst[0]] = v0;
+            if (it0 + 32 < items) vb[dst[1]] = v1;
           }
-          bool out;
-          const double v0 = field_value_fast<MODE>(g, pg, pal, p[0], out);
-          const double v1 = field_value_fast<MODE>(g, pg, pal, p[1], out);
-          vb[dst[0]] = v0;
-          if (it0 + 32 < items) vb[dst[1]] = v1;
         }
         __syncwarp();
         // geo_score of each neighbour in the group (grid.cpp:97-101)
