@@ -105,10 +105,12 @@ __device__ __forceinline__ int mvar_off(int v, int u, int m) {
 __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, const double *base, const uint16_t *ta,
                                         const uint16_t *tb, const uint32_t *tm, const double *Mcur,
                                         const double *sccur, double *out) {
+  #pragma unroll 1
   for (int u = t; u < m; ++u) {
     const int a = ta[u], b = tb[u];
     d3 ea = ld3(base + 3 * a), eb = ld3(base + 3 * b);
     const uint32_t ma = tm[a], mb = tm[b];
+    #pragma unroll 1
     for (int w = 0; w < u; ++w) {
       const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
       if ((ma >> w) & 1u) ea = torsion_apply(M, ea);
@@ -206,9 +208,11 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
       continue;
     }
     // torsioned frame (search.cpp:115)
+    #pragma unroll 1
     for (int a = lane; a < N; a += 32) {
       d3 x = ld3(base + 3 * a);
       const uint32_t mask = tm[a];
+      #pragma unroll 1
       for (int u = 0; u < m; ++u)
         if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
       st3(tors + 3 * a, x);
@@ -262,6 +266,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         S[S_GEO] = A.pose_in[8 * l + 7];
       } else {
         double acc = 0.0;
+        #pragma unroll 1
         for (int h = 0; h < n; ++h) acc += vcur[h];
         S[S_GEO] = acc;
       }
@@ -279,9 +284,12 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
       if (row < 2) {
         const int size4 = (N - 1) & ~3;
         int i = 1;
+        #pragma unroll 1
         for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
+        #pragma unroll 1
         for (; i < N; ++i) p = p + val(i);
       } else {
+        #pragma unroll 1
         for (int i = 1; i < N; ++i) p = p + val(i);
       }
       S[S_PIV + row] = p / (double)N;
@@ -395,6 +403,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
               const int a = hl[h];
               d3 x = ld3(base + 3 * a);
               const uint32_t mask = tm[a];
+              #pragma unroll 1
               for (int u = 0; u < m; ++u) {
                 if (!((mask >> u) & 1u)) continue;
                 x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
@@ -415,9 +424,11 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
           const double *row = vb + lane * nmax;
           double acc = 0.0;
           if (grp == 0) {
+            #pragma unroll 4
             for (int h = 0; h < n; ++h) acc += row[h];
           } else {
             const int t = tlo + (lane >> 1);
+            #pragma unroll 4
             for (int h = 0; h < n; ++h) acc += ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
           }
           scores[lane] = acc;
@@ -460,6 +471,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         } else {
           const int v = bj - 12, t = v >> 1;
           const double sign = (v & 1) ? -1.0 : 1.0;
+          #pragma unroll 1
           for (int i = lane; i < 12 * (m - t); i += 32) Mcur[12 * t + i] = Mvar[mvar_off(v, t, m) + i];
           if (lane == 0) {
             ang[t] = ang[t] + sign * step_q;
@@ -469,14 +481,17 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
           if (lane < 2) cvalid[2 * t + lane] = 0;
           mvar_valid = false;
           __syncwarp();
+          #pragma unroll 1
           for (int a = lane; a < N; a += 32) {
             d3 x = ld3(base + 3 * a);
             const uint32_t mask = tm[a];
+            #pragma unroll 1
             for (int u = 0; u < m; ++u)
               if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
             st3(tors + 3 * a, x);
           }
         }
+        #pragma unroll 1
         for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
         if (lane == 0) S[S_GEO] = bv;
         __syncwarp();
@@ -488,9 +503,12 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
           if (row < 2) {
             const int size4 = (N - 1) & ~3;
             int i = 1;
+            #pragma unroll 1
             for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
+            #pragma unroll 1
             for (; i < N; ++i) p = p + val(i);
           } else {
+            #pragma unroll 1
             for (int i = 1; i < N; ++i) p = p + val(i);
           }
           S[S_PIV + row] = p / (double)N;
