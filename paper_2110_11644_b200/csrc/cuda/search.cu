@@ -36,6 +36,10 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kGroup = 16;  // neighbours per group (>= 12)
+#ifndef VS_SEARCH_ILP
+#define VS_SEARCH_ILP 2  // samples in flight per lane in the item loops
+#endif
+constexpr int kIlp = VS_SEARCH_ILP;
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
@@ -44,13 +48,6 @@ __device__ __forceinline__ void st3(double *p, d3 v) {
   p[0] = v.x;
   p[1] = v.y;
   p[2] = v.z;
-}
-
-// Row `row` of rigid_col (the reference's 3xN apply_rigid, Appendix A item 4).
-__device__ __forceinline__ double rigid_row(const double *r, const double *t, d3 v, int col, int row) {
-  const double a0 = r[3 * row] * v.x, a1 = r[3 * row + 1] * v.y, a2 = r[3 * row + 2] * v.z;
-  const bool packet = (col & 1) == 0 ? row < 2 : row > 0;
-  return (packet ? (a0 + a1) + a2 : a0 + (a1 + a2)) + t[row];
 }
 
 __device__ __noinline__ void sincos_cr_dev(double a, double *s, double *c) { vs_crtrig::sincos_cr(a, s, c); }
@@ -121,6 +118,16 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
     if (!torsion_setup(ea, eb, s, c, out + 12 * (u - t))) return false;
   }
   return true;
+}
+
+// Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
+// the transformed coordinates to `scratch`, then three lanes run the
+// Eigen-order row sums (dmath.cuh centroid_row).  One out-of-line copy.
+__device__ __noinline__ void compute_pivot(double *scratch, const double *tors, double *S, int N, int lane) {
+  for (int a = lane; a < N; a += 32) st3(scratch + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
+  __syncwarp();
+  if (lane < 3) S[S_PIV + lane] = centroid_row(scratch, N, lane);
+  __syncwarp();
 }
 
 template <int MODE>
@@ -273,28 +280,12 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
     }
     if (!ls_mode) evals += (unsigned long long)n;
     // pivot of the start pose: centroid of its conformation (search.cpp:124)
-    if (lane < 3) {
-      const int row = lane;
-      double p;
-      auto val = [&](int a) -> double {
-        if (ls_mode) return A.conf_in[3 * ((size_t)a0 + a) + row];
-        return rigid_row(S + S_R, S + S_T, ld3(tors + 3 * a), a, row);
-      };
-      p = val(0);
-      if (row < 2) {
-        const int size4 = (N - 1) & ~3;
-        int i = 1;
-        #pragma unroll 1
-        for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
-        #pragma unroll 1
-        for (; i < N; ++i) p = p + val(i);
-      } else {
-        #pragma unroll 1
-        for (int i = 1; i < N; ++i) p = p + val(i);
-      }
-      S[S_PIV + row] = p / (double)N;
+    if (ls_mode) {
+      if (lane < 3) S[S_PIV + lane] = centroid_row(A.conf_in + 3 * (size_t)a0, N, lane);
+      __syncwarp();
+    } else {
+      compute_pivot(vb, tors, S, N, lane);
     }
-    __syncwarp();
 
     // ---- local_search (search.cpp:121-191)
     int level = 0, n_iter = 0, n_adopt = 0;
@@ -370,11 +361,11 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         // rigid and the torsion neighbours run in separate compact loops.
         if (grp == 0) {
           const float rn = 1.0f / (float)n;
-          for (int it0 = lane; it0 < items; it0 += 64) {
-            d3 p[2];
-            int dst[2];
+          for (int it0 = lane; it0 < items; it0 += 32 * kIlp) {
+            d3 p[kIlp];
+            int dst[kIlp];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kIlp; ++q) {
               const int it = min(it0 + 32 * q, items - 1);
               int j = __float2int_rz((float)it * rn);
               j -= (j * n > it) ? 1 : 0;
@@ -385,19 +376,21 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
               p[q] = rigid_col(X, X + 9, ld3(tors + 3 * a), a);
               dst[q] = j * nmax + h;
             }
+            double val[kIlp];
             bool out;
-            const double v0 = field_value_fast<MODE>(g, pg, pal, p[0], out);
-            const double v1 = field_value_fast<MODE>(g, pg, pal, p[1], out);
-            vb[dst[0]] = v0;
-            if (it0 + 32 < items) vb[dst[1]] = v1;
+#pragma unroll
+            for (int q = 0; q < kIlp; ++q) val[q] = field_value_fast<MODE>(g, pg, pal, p[q], out);
+#pragma unroll
+            for (int q = 0; q < kIlp; ++q)
+              if (it0 + 32 * q < items) vb[dst[q]] = val[q];
           }
         } else {
           const uint16_t *ti = titems + 2 * doff[tlo];
-          for (int it0 = lane; it0 < items; it0 += 64) {
-            d3 p[2];
-            int dst[2];
+          for (int it0 = lane; it0 < items; it0 += 32 * kIlp) {
+            d3 p[kIlp];
+            int dst[kIlp];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kIlp; ++q) {
               const int e = ti[min(it0 + 32 * q, items - 1)];
               const int v = e >> 8, h = e & 255, t = v >> 1;
               const int a = hl[h];
@@ -411,11 +404,13 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
               p[q] = rigid_col(S + S_R, S + S_T, x, a);
               dst[q] = (v - 2 * tlo) * nmax + h;
             }
+            double val[kIlp];
             bool out;
-            const double v0 = field_value_fast<MODE>(g, pg, pal, p[0], out);
-            const double v1 = field_value_fast<MODE>(g, pg, pal, p[1], out);
-            vb[dst[0]] = v0;
-            if (it0 + 32 < items) vb[dst[1]] = v1;
+#pragma unroll
+            for (int q = 0; q < kIlp; ++q) val[q] = field_value_fast<MODE>(g, pg, pal, p[q], out);
+#pragma unroll
+            for (int q = 0; q < kIlp; ++q)
+              if (it0 + 32 * q < items) vb[dst[q]] = val[q];
           }
         }
         __syncwarp();
@@ -495,24 +490,8 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
         if (lane == 0) S[S_GEO] = bv;
         __syncwarp();
-        // new pivot = centroid of the adopted conformation
-        if (lane < 3) {
-          const int row = lane;
-          auto val = [&](int a) -> double { return rigid_row(S + S_R, S + S_T, ld3(tors + 3 * a), a, row); };
-          double p = val(0);
-          if (row < 2) {
-            const int size4 = (N - 1) & ~3;
-            int i = 1;
-            #pragma unroll 1
-            for (; i < size4; i += 4) p = p + ((val(i) + val(i + 1)) + (val(i + 2) + val(i + 3)));
-            #pragma unroll 1
-            for (; i < N; ++i) p = p + val(i);
-          } else {
-            #pragma unroll 1
-            for (int i = 1; i < N; ++i) p = p + val(i);
-          }
-          S[S_PIV + row] = p / (double)N;
-        }
+        // new pivot = centroid of the adopted conformation (vb is free here)
+        compute_pivot(vb, tors, S, N, lane);
       } else {
         if (lane == 0) {
           S[S_STEPT] = S[S_STEPT] * 0.5;
@@ -569,7 +548,7 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   A.o_Mcur = take(12 * mm);
   A.o_Mvar = take(12 * mm * (mm + 1));
   A.o_Rj = take(16 * 12);
-  A.o_vb = take(kGroup * nm);
+  A.o_vb = take(kGroup * nm > 3 * Nm ? kGroup * nm : 3 * Nm);  // also the pivot scratch
   A.o_vbest = take(nm);
   A.o_vcur = take(nm);
   A.o_scores = take(kGroup);

@@ -11,7 +11,8 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libvsdock.so")
+# VSDOCK_LIB overrides the library path (development A/B builds only).
+LIB_PATH = os.environ.get("VSDOCK_LIB") or os.path.join(HERE, "_lib", "libvsdock.so")
 
 _d = C.POINTER(C.c_double)
 _u64 = C.POINTER(C.c_uint64)
