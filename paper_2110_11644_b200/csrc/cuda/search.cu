@@ -37,7 +37,7 @@ namespace {
 constexpr int kWarps = 4;
 constexpr int kGroup = 16;  // neighbours per group (>= 12)
 #ifndef VS_SEARCH_ILP
-#define VS_SEARCH_ILP 2  // samples in flight per lane in the item loops
+#define VS_SEARCH_ILP 1  // samples in flight per lane (1: smallest hot code, fastest measured)
 #endif
 constexpr int kIlp = VS_SEARCH_ILP;
 constexpr double kPi = 3.14159265358979323846;
@@ -359,50 +359,43 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         }
         // Two items per lane per step (independent gathers in flight); the
         // rigid and the torsion neighbours run in separate compact loops.
-        if (grp == 0) {
+        // One compact loop for both kinds of neighbour (a single inlined
+        // sampler keeps the hot instruction footprint small: the search is
+        // instruction-fetch bound when warps at different phases share an SM).
+        {
           const float rn = 1.0f / (float)n;
-          for (int it0 = lane; it0 < items; it0 += 32 * kIlp) {
-            d3 p[kIlp];
-            int dst[kIlp];
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q) {
-              const int it = min(it0 + 32 * q, items - 1);
-              int j = __float2int_rz((float)it * rn);
-              j -= (j * n > it) ? 1 : 0;
-              j += ((j + 1) * n <= it) ? 1 : 0;
-              const int h = it - j * n;
-              const int a = hl[h];
-              const double *X = Rj + 16 * j;
-              p[q] = rigid_col(X, X + 9, ld3(tors + 3 * a), a);
-              dst[q] = j * nmax + h;
-            }
-            double val[kIlp];
-            bool out;
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q) val[q] = field_value_fast<MODE>(g, pg, pal, p[q], out);
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q)
-              if (it0 + 32 * q < items) vb[dst[q]] = val[q];
-          }
-        } else {
           const uint16_t *ti = titems + 2 * doff[tlo];
           for (int it0 = lane; it0 < items; it0 += 32 * kIlp) {
             d3 p[kIlp];
             int dst[kIlp];
 #pragma unroll
             for (int q = 0; q < kIlp; ++q) {
-              const int e = ti[min(it0 + 32 * q, items - 1)];
-              const int v = e >> 8, h = e & 255, t = v >> 1;
+              const int it = min(it0 + 32 * q, items - 1);
+              int h, j, t = m, v = 0;
+              if (grp == 0) {
+                j = __float2int_rz((float)it * rn);
+                j -= (j * n > it) ? 1 : 0;
+                j += ((j + 1) * n <= it) ? 1 : 0;
+                h = it - j * n;
+              } else {
+                const int e = ti[it];
+                v = e >> 8;
+                h = e & 255;
+                t = v >> 1;
+                j = v - 2 * tlo;
+              }
               const int a = hl[h];
-              d3 x = ld3(base + 3 * a);
-              const uint32_t mask = tm[a];
+              d3 x = ld3((grp == 0 ? tors : base) + 3 * a);
+              const uint32_t mask = grp == 0 ? 0u : tm[a];
               #pragma unroll 1
               for (int u = 0; u < m; ++u) {
                 if (!((mask >> u) & 1u)) continue;
                 x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
               }
-              p[q] = rigid_col(S + S_R, S + S_T, x, a);
-              dst[q] = (v - 2 * tlo) * nmax + h;
+              const double *X = grp == 0 ? Rj + 16 * j : S + S_R;
+              const double *T = grp == 0 ? X + 9 : S + S_T;
+              p[q] = rigid_col(X, T, x, a);
+              dst[q] = j * nmax + h;
             }
             double val[kIlp];
             bool out;
