@@ -81,7 +81,7 @@ struct vs_context {
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
   DevBuf results, best_ang, best_conf, counters, spin, fibq;
-  DevBuf aux0, aux1, aux2, aux3, search_args;
+  DevBuf aux0, aux1, aux2, aux3, search_args, lig_index;
 };
 
 struct vs_pocket {
@@ -284,6 +284,7 @@ struct Staged {
   int Nmax = 0, nmax = 0, mmax = 0;
   int atoms = 0, torsions = 0;
   std::vector<int> atom_off, bond_off, tors_off, right_off, ditem_base;
+  std::vector<int> lN, ln, lm;  // per ligand: atoms, heavy atoms, torsions
 };
 
 template <typename T>
@@ -309,6 +310,9 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   st.ditem_base.resize(n + 1);
   st.right_off.resize(T1 - T0 + 1);
   st.Nmax = st.nmax = st.mmax = 0;
+  st.lN.assign(n, 0);
+  st.ln.assign(n, 0);
+  st.lm.assign(n, 0);
   int dbase = 0;
   for (int i = 0; i <= n; ++i) {
     st.atom_off[i] = in->atom_offset[l0 + i] - A0;
@@ -320,6 +324,9 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
       const int m = in->torsion_offset[l0 + i + 1] - in->torsion_offset[l0 + i];
       int h = 0;
       for (int a = in->atom_offset[l0 + i]; a < in->atom_offset[l0 + i + 1]; ++a) h += in->is_heavy[a] ? 1 : 0;
+      st.lN[i] = N;
+      st.ln[i] = h;
+      st.lm[i] = m;
       if (N <= VS_MAX_ATOMS && m <= VS_MAX_TORSIONS && h <= VS_MAX_HEAVY) {
         st.Nmax = std::max(st.Nmax, N);
         st.mmax = std::max(st.mmax, m);
@@ -751,8 +758,44 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(vsd::launch_flatten(st.b, cfg->flatten_max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
     CUDA_TRY(ctx->search_args.ensure(vsd::search_args_bytes()));
-    CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax, ctx->num_sms,
-                                ctx->stream, nullptr, ctx->search_args.p));
+    {
+      // Size buckets: ligands grouped by how many 4-warp search CTAs per SM
+      // their shared-memory footprint allows, each bucket launched with its
+      // own maxima so one large ligand does not shrink everyone's occupancy.
+      std::vector<std::vector<int>> buckets(5);
+      for (int i = 0; i < st.n; ++i) {
+        if (st.lN[i] > VS_MAX_ATOMS || st.lm[i] > VS_MAX_TORSIONS || st.ln[i] > VS_MAX_HEAVY) {
+          buckets[4].push_back(i);  // rejected by k_setup; cheapest launch
+          continue;
+        }
+        const size_t bytes = vsd::search_smem_bytes(st.lN[i], st.ln[i], st.lm[i]);
+        const int per_sm = static_cast<int>(std::min<size_t>(4, (227 * 1024) / std::max<size_t>(bytes, 1)));
+        buckets[std::max(1, per_sm) - 1].push_back(i);
+      }
+      std::vector<int> order;
+      std::vector<std::pair<int, int>> ranges;
+      for (auto &bk : buckets) {
+        ranges.push_back({static_cast<int>(order.size()), static_cast<int>(bk.size())});
+        order.insert(order.end(), bk.begin(), bk.end());
+      }
+      if ((rc = h2d(ctx->lig_index, order.data(), order.size(), ctx->stream))) return rc;
+      for (size_t bi = 0; bi < buckets.size(); ++bi) {
+        if (buckets[bi].empty()) continue;
+        int Nm = 1, nm = 1, mm = 1;
+        for (int i : buckets[bi])
+          if (bi < 4) {
+            Nm = std::max(Nm, st.lN[i]);
+            nm = std::max(nm, st.ln[i]);
+            mm = std::max(mm, st.lm[i]);
+          }
+        CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
+        CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), Nm, nm, mm, ctx->num_sms, ctx->stream,
+                                    nullptr, ctx->search_args.p, ctx->lig_index.as<int>() + ranges[bi].first,
+                                    ranges[bi].second));
+        ++ctx->last_launches;
+      }
+      --ctx->last_launches;  // counted once below with the fixed launches
+    }
     CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
     CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));

@@ -111,9 +111,12 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
                            cudaStream_t s);
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
-                          int num_sms, cudaStream_t s, int *launches, void *args_buf);
+                          int num_sms, cudaStream_t s, int *launches, void *args_buf,
+                          const int *lig_index = nullptr, int n_lig = 0);
 // device buffer size the search launchers need for their argument block
 size_t search_args_bytes();
+// dynamic shared memory of one k_search CTA for the given ligand maxima
+size_t search_smem_bytes(int N, int n, int m);
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s);
 // sub-API kernels

@@ -36,10 +36,6 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kGroup = 16;  // neighbours per group (>= 12)
-#ifndef VS_SEARCH_ILP
-#define VS_SEARCH_ILP 1  // samples in flight per lane (1: smallest hot code, fastest measured)
-#endif
-constexpr int kIlp = VS_SEARCH_ILP;
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
@@ -82,6 +78,7 @@ struct search_args {
   const double *conf_in;
   int *work;
   int n_items;
+  const int *lig_index;  // bucket launches: item / k -> ligand (NULL: identity)
   int Nmax, nmax, mmax;
   int warp_doubles;
   int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints;
@@ -167,7 +164,9 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
     if (lane == 0) item = atomicAdd(A.work, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= A.n_items) break;
-    const int l = item / k, r = item - l * k;
+    const int li = item / k, r = item - li * k;
+    const int l = A.lig_index ? A.lig_index[li] : li;
+    item = l * k + r;  // global item index of the outputs
     const lig_meta meta = b.meta[l];
     if (meta.status != VS_LIG_OK) {
       if (lane == 0) A.o.status[item] = meta.status;
@@ -359,51 +358,37 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         }
         // Two items per lane per step (independent gathers in flight); the
         // rigid and the torsion neighbours run in separate compact loops.
-        // One compact loop for both kinds of neighbour (a single inlined
-        // sampler keeps the hot instruction footprint small: the search is
-        // instruction-fetch bound when warps at different phases share an SM).
-        {
+        // Rigid and torsion neighbours run in separate compact loops, one
+        // sample per lane per step: the search is instruction-fetch bound
+        // when warps at different phases share an SM, so the hot code is
+        // kept small (measured: 1 sample in flight beats 2 or 3).
+        if (grp == 0) {
           const float rn = 1.0f / (float)n;
-          const uint16_t *ti = titems + 2 * doff[tlo];
-          for (int it0 = lane; it0 < items; it0 += 32 * kIlp) {
-            d3 p[kIlp];
-            int dst[kIlp];
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q) {
-              const int it = min(it0 + 32 * q, items - 1);
-              int h, j, t = m, v = 0;
-              if (grp == 0) {
-                j = __float2int_rz((float)it * rn);
-                j -= (j * n > it) ? 1 : 0;
-                j += ((j + 1) * n <= it) ? 1 : 0;
-                h = it - j * n;
-              } else {
-                const int e = ti[it];
-                v = e >> 8;
-                h = e & 255;
-                t = v >> 1;
-                j = v - 2 * tlo;
-              }
-              const int a = hl[h];
-              d3 x = ld3((grp == 0 ? tors : base) + 3 * a);
-              const uint32_t mask = grp == 0 ? 0u : tm[a];
-              #pragma unroll 1
-              for (int u = 0; u < m; ++u) {
-                if (!((mask >> u) & 1u)) continue;
-                x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
-              }
-              const double *X = grp == 0 ? Rj + 16 * j : S + S_R;
-              const double *T = grp == 0 ? X + 9 : S + S_T;
-              p[q] = rigid_col(X, T, x, a);
-              dst[q] = j * nmax + h;
-            }
-            double val[kIlp];
+          for (int it = lane; it < items; it += 32) {
+            int j = __float2int_rz((float)it * rn);
+            j -= (j * n > it) ? 1 : 0;
+            j += ((j + 1) * n <= it) ? 1 : 0;
+            const int h = it - j * n;
+            const int a = hl[h];
+            const double *X = Rj + 16 * j;
             bool out;
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q) val[q] = field_value_fast<MODE>(g, pg, pal, p[q], out);
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q)
-              if (it0 + 32 * q < items) vb[dst[q]] = val[q];
+            vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(X, X + 9, ld3(tors + 3 * a), a), out);
+          }
+        } else {
+          const uint16_t *ti = titems + 2 * doff[tlo];
+          for (int it = lane; it < items; it += 32) {
+            const int e = ti[it];
+            const int v = e >> 8, h = e & 255, t = v >> 1;
+            const int a = hl[h];
+            d3 x = ld3(base + 3 * a);
+            const uint32_t mask = tm[a];
+            #pragma unroll 1
+            for (int u = 0; u < m; ++u) {
+              if (!((mask >> u) & 1u)) continue;
+              x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
+            }
+            bool out;
+            vb[(v - 2 * tlo) * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, x, a), out);
           }
         }
         __syncwarp();
@@ -529,28 +514,52 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
 
 namespace {
 
-cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
-  const int Nm = A.Nmax, nm = A.nmax, mm = A.mmax;
+struct Layout {
+  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints, total;
+};
+
+Layout layout(int Nm, int nm, int mm) {
+  Layout L{};
   int o = 0;
   auto take = [&](int n) {
     const int at = o;
     o += (n + 1) & ~1;  // keep 16-byte alignment
     return at;
   };
-  A.o_tors = take(3 * Nm);
-  A.o_Mcur = take(12 * mm);
-  A.o_Mvar = take(12 * mm * (mm + 1));
-  A.o_Rj = take(16 * 12);
-  A.o_vb = take(kGroup * nm > 3 * Nm ? kGroup * nm : 3 * Nm);  // also the pivot scratch
-  A.o_vbest = take(nm);
-  A.o_vcur = take(nm);
-  A.o_scores = take(kGroup);
-  A.o_cache = take(4 * mm);
-  A.o_ang = take(mm);
-  A.o_sccur = take(2 * mm);
-  A.o_state = take(S_N);
-  A.o_ints = take((nm + Nm + 2 * mm + 3) / 2 + 1);
-  A.warp_doubles = o;
+  L.o_tors = take(3 * Nm);
+  L.o_Mcur = take(12 * mm);
+  L.o_Mvar = take(12 * mm * (mm + 1));
+  L.o_Rj = take(16 * 12);
+  L.o_vb = take(kGroup * nm > 3 * Nm ? kGroup * nm : 3 * Nm);  // also the pivot scratch
+  L.o_vbest = take(nm);
+  L.o_vcur = take(nm);
+  L.o_scores = take(kGroup);
+  L.o_cache = take(4 * mm);
+  L.o_ang = take(mm);
+  L.o_sccur = take(2 * mm);
+  L.o_state = take(S_N);
+  L.o_ints = take((nm + 2 * mm + 3) / 2 + 1);
+  L.total = o;
+  return L;
+}
+
+cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
+  const Layout L = layout(A.Nmax, A.nmax, A.mmax);
+  A.o_tors = L.o_tors;
+  A.o_Mcur = L.o_Mcur;
+  A.o_Mvar = L.o_Mvar;
+  A.o_Rj = L.o_Rj;
+  A.o_vb = L.o_vb;
+  A.o_vbest = L.o_vbest;
+  A.o_vcur = L.o_vcur;
+  A.o_scores = L.o_scores;
+  A.o_cache = L.o_cache;
+  A.o_ang = L.o_ang;
+  A.o_sccur = L.o_sccur;
+  A.o_state = L.o_state;
+  A.o_ints = L.o_ints;
+  A.warp_doubles = L.total;
+  const int o = L.total;
   const size_t smem = (size_t)(16 + o * kWarps) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const void *fn = A.pg.mode == 1 ? (const void *)k_search<1>
@@ -580,9 +589,15 @@ void set_lattice_table_search(const double *sc72) { cudaMemcpyToSymbol(c_lattice
 
 size_t search_args_bytes() { return sizeof(search_args); }
 
+size_t search_smem_bytes(int N, int n, int m) {
+  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1);
+  return (size_t)(16 + L.total * kWarps) * sizeof(double);
+}
+
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
-                          int num_sms, cudaStream_t s, int *launches, void *args_buf) {
+                          int num_sms, cudaStream_t s, int *launches, void *args_buf, const int *lig_index,
+                          int n_lig) {
   (void)args_buf;
   search_args A{};
   A.b = b;
@@ -592,7 +607,8 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
   A.f = f;
   A.o = o;
   A.work = work_counter;
-  A.n_items = b.n_lig * c.k;
+  A.lig_index = lig_index;
+  A.n_items = (lig_index ? n_lig : b.n_lig) * c.k;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
