@@ -149,8 +149,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
   double *sccur = W + A.o_sccur;
   double *S = W + A.o_state;
   uint32_t *dm = reinterpret_cast<uint32_t *>(W + A.o_ints);
-  int *hidx = reinterpret_cast<int *>(dm + A.nmax);
-  int *cvalid = hidx + A.Nmax;
+  int *cvalid = reinterpret_cast<int *>(dm + A.nmax);
 
   const batch_dev &b = A.b;
   const grid_view &g = A.p.g;
@@ -184,10 +183,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
     unsigned long long evals = 0;
 
     // ---- per-ligand tables
-    for (int a = lane; a < N; a += 32) hidx[a] = -1;
-    __syncwarp();
     for (int h = lane; h < n; h += 32) {
-      hidx[hl[h]] = h;
       dm[h] = b.heavy_dmask[a0 + h];
     }
     for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
