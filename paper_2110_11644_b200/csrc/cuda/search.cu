@@ -359,16 +359,17 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         // when warps at different phases share an SM, so the hot code is
         // kept small (measured: 1 sample in flight beats 2 or 3).
         if (grp == 0) {
-          const float rn = 1.0f / (float)n;
-          for (int it = lane; it < items; it += 32) {
-            int j = __float2int_rz((float)it * rn);
-            j -= (j * n > it) ? 1 : 0;
-            j += ((j + 1) * n <= it) ? 1 : 0;
-            const int h = it - j * n;
+          // rigid neighbours: lane = heavy atom, loop over the 12 transforms
+          // (their matrices are warp-uniform shared-memory broadcasts)
+          for (int h = lane; h < n; h += 32) {
             const int a = hl[h];
-            const double *X = Rj + 16 * j;
-            bool out;
-            vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(X, X + 9, ld3(tors + 3 * a), a), out);
+            const d3 x = ld3(tors + 3 * a);
+            #pragma unroll 1
+            for (int j = 0; j < 12; ++j) {
+              const double *X = Rj + 16 * j;
+              bool out;
+              vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(X, X + 9, x, a), out);
+            }
           }
         } else {
           const uint16_t *ti = titems + 2 * doff[tlo];
