@@ -360,7 +360,7 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   CUDA_TRY(ctx->d_count.ensure(4 * nt));
   CUDA_TRY(ctx->d_off.ensure(4 * nt));
   CUDA_TRY(ctx->ditems.ensure(2 * static_cast<size_t>(std::max(dbase, 1))));
-  CUDA_TRY(ctx->titems.ensure(4 * static_cast<size_t>(std::max(dbase, 1))));
+  CUDA_TRY(ctx->titems.ensure(8 * static_cast<size_t>(std::max(dbase, 1))));
   vsd::batch_dev &b = st.b;
   b.n_lig = n;
   b.atom_off = ctx->atom_off.as<int>();
@@ -384,7 +384,7 @@ vs_status stage(vs_context *ctx, const vs_ligand_batch *in, int l0, int l1, Stag
   b.d_count = ctx->d_count.as<int>();
   b.d_off = ctx->d_off.as<int>();
   b.ditems = ctx->ditems.as<uint16_t>();
-  b.titems = ctx->titems.as<uint16_t>();
+  b.titems = ctx->titems.as<uint32_t>();
   return VS_OK;
 }
 
@@ -755,21 +755,27 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(cudaEventRecord(ctx->evs[0], ctx->stream));
     CUDA_TRY(vsd::launch_setup(st.b, k, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[1], ctx->stream));
+    // per-ligand sizes for the search buckets come back while flatten runs
+    std::vector<vsd::lig_meta> meta(static_cast<size_t>(std::max(st.n, 1)));
+    CUDA_TRY(cudaMemcpyAsync(meta.data(), st.b.meta, sizeof(vsd::lig_meta) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
     CUDA_TRY(vsd::launch_flatten(st.b, cfg->flatten_max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
     CUDA_TRY(ctx->search_args.ensure(vsd::search_args_bytes()));
+    CUDA_TRY(cudaEventSynchronize(ctx->ev1));
     {
       // Size buckets: ligands grouped by how many 4-warp search CTAs per SM
       // their shared-memory footprint allows, each bucket launched with its
       // own maxima so one large ligand does not shrink everyone's occupancy.
       std::vector<std::vector<int>> buckets(5);
       for (int i = 0; i < st.n; ++i) {
-        if (st.lN[i] > VS_MAX_ATOMS || st.lm[i] > VS_MAX_TORSIONS || st.ln[i] > VS_MAX_HEAVY) {
-          buckets[4].push_back(i);  // rejected by k_setup; cheapest launch
+        const vsd::lig_meta &mt = meta[static_cast<size_t>(i)];
+        if (mt.status != VS_LIG_OK) {
+          buckets[4].push_back(i);  // rejected by k_setup: the kernel only records the status
           continue;
         }
-        const size_t bytes = vsd::search_smem_bytes(st.lN[i], st.ln[i], st.lm[i]);
-        const int per_sm = static_cast<int>(std::min<size_t>(4, (227 * 1024) / std::max<size_t>(bytes, 1)));
+        const size_t bytes = vsd::search_smem_bytes(mt.n_atoms, mt.n_heavy, mt.m, mt.d_total) + 1024;
+        const int per_sm = static_cast<int>(std::min<size_t>(4, (228 * 1024) / std::max<size_t>(bytes, 1)));
         buckets[std::max(1, per_sm) - 1].push_back(i);
       }
       std::vector<int> order;
@@ -781,17 +787,19 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
       if ((rc = h2d(ctx->lig_index, order.data(), order.size(), ctx->stream))) return rc;
       for (size_t bi = 0; bi < buckets.size(); ++bi) {
         if (buckets[bi].empty()) continue;
-        int Nm = 1, nm = 1, mm = 1;
-        for (int i : buckets[bi])
-          if (bi < 4) {
-            Nm = std::max(Nm, st.lN[i]);
-            nm = std::max(nm, st.ln[i]);
-            mm = std::max(mm, st.lm[i]);
-          }
+        int Nm = 1, nm = 1, mm = 1, dm = 1;
+        for (int i : buckets[bi]) {
+          const vsd::lig_meta &mt = meta[static_cast<size_t>(i)];
+          if (mt.status != VS_LIG_OK) continue;
+          Nm = std::max(Nm, mt.n_atoms);
+          nm = std::max(nm, mt.n_heavy);
+          mm = std::max(mm, mt.m);
+          dm = std::max(dm, mt.d_total);
+        }
         CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
         CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), Nm, nm, mm, ctx->num_sms, ctx->stream,
                                     nullptr, ctx->search_args.p, ctx->lig_index.as<int>() + ranges[bi].first,
-                                    ranges[bi].second));
+                                    ranges[bi].second, dm));
         ++ctx->last_launches;
       }
       --ctx->last_launches;  // counted once below with the fixed launches

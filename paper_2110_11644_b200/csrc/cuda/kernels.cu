@@ -48,7 +48,7 @@ __global__ void k_setup(batch_dev b, int restarts) {
   const int a0 = b.atom_off[l], N = b.atom_off[l + 1] - a0;
   const int b0 = b.bond_off[l], nb = b.bond_off[l + 1] - b0;
   const int t0 = b.tors_off[l], m = b.tors_off[l + 1] - t0;
-  lig_meta meta{N, 0, m, VS_LIG_OK, 0, 0};
+  lig_meta meta{N, 0, m, VS_LIG_OK, 0, 0, 0};
   // apply_torsion's index checks (transform.cpp:56-57, 66-67) fire in the
   // first flatten pass, before any coordinate is used.
   if (m > VS_MAX_TORSIONS) meta.status = VS_LIG_TOO_LARGE;
@@ -116,15 +116,31 @@ __global__ void k_setup(batch_dev b, int restarts) {
         ++cnt;
       }
     }
+    // Order D_t by the atoms' remaining torsion chain (right-set membership
+    // of torsions >= t), so that neighbouring search lanes apply the same
+    // rotations (less divergence).  Stable insertion sort, lists are short.
+    uint16_t *dl = b.ditems + base + off;
+    for (int i = 1; i < cnt; ++i) {
+      const uint16_t hv = dl[i];
+      const uint32_t key = b.atom_tmask[a0 + b.heavy_list[a0 + hv]] >> t;
+      int j = i - 1;
+      while (j >= 0 && (b.atom_tmask[a0 + b.heavy_list[a0 + dl[j]]] >> t) > key) {
+        dl[j + 1] = dl[j];
+        --j;
+      }
+      dl[j + 1] = hv;
+    }
     b.d_count[t0 + t] = cnt;
     b.d_off[t0 + t] = off;
-    // the 2*cnt search items of neighbours (t,+) and (t,-), in that order
+    // the 2*cnt search items of neighbours (t,+) and (t,-), in that order;
+    // bits 14+ index the atom's stage-t position in the search's prefix list
     for (int s = 0; s < 2; ++s)
       for (int i = 0; i < cnt; ++i)
         b.titems[2 * base + 2 * off + s * cnt + i] =
-            (uint16_t)(((2 * t + s) << 8) | b.ditems[base + off + i]);
+            (uint32_t)dl[i] | ((uint32_t)(2 * t + s) << 8) | ((uint32_t)(off + i) << 14);
     off += cnt;
   }
+  meta.d_total = off;
   b.meta[l] = meta;
 }
 

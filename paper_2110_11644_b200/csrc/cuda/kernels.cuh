@@ -18,6 +18,7 @@ struct lig_meta {
   int status;   // vs_ligand_status
   int r_all;    // sum_t |right_set(t)|          (counter model, Appendix B)
   int r_heavy;  // sum_t |right_set(t) ∩ heavy|
+  int d_total;  // sum_t |D_t ∩ heavy| (stage-t prefix positions the search keeps)
 };
 
 // Device copy of one batch (vs_ligand_batch) plus derived arrays.
@@ -45,7 +46,7 @@ struct batch_dev {
   int *d_count;            // torsions: |D_t ∩ heavy|
   int *d_off;              // torsions: offset of D_t items in the ligand list
   uint16_t *ditems;        // ditem_base[l] + ...: heavy indices of D_t items
-  uint16_t *titems;        // 2*ditem_base[l] + ...: torsion-neighbour items ((2t+s) << 8) | h
+  uint32_t *titems;        // 2*ditem_base[l] + ...: torsion-neighbour items h | (2t+s) << 8 | pd << 14
 };
 
 struct pocket_dev {
@@ -112,11 +113,11 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf,
-                          const int *lig_index = nullptr, int n_lig = 0);
+                          const int *lig_index = nullptr, int n_lig = 0, int dmax = 0);
 // device buffer size the search launchers need for their argument block
 size_t search_args_bytes();
 // dynamic shared memory of one k_search CTA for the given ligand maxima
-size_t search_smem_bytes(int N, int n, int m);
+size_t search_smem_bytes(int N, int n, int m, int dtot);
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s);
 // sub-API kernels
