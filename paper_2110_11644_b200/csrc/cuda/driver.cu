@@ -774,9 +774,11 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
           buckets[4].push_back(i);  // rejected by k_setup: the kernel only records the status
           continue;
         }
+        // warps per SM this ligand's footprint allows (registers cap it at 16)
         const size_t bytes = vsd::search_smem_bytes(mt.n_atoms, mt.n_heavy, mt.m, mt.d_total) + 1024;
-        const int per_sm = static_cast<int>(std::min<size_t>(4, (228 * 1024) / std::max<size_t>(bytes, 1)));
-        buckets[std::max(1, per_sm) - 1].push_back(i);
+        const int ctas = static_cast<int>((228 * 1024) / std::max<size_t>(bytes, 1));
+        const int warps = std::min(16, ctas * vsd::search_warps_per_cta());
+        buckets[warps >= 16 ? 3 : (warps >= 12 ? 2 : (warps >= 8 ? 1 : 0))].push_back(i);
       }
       std::vector<int> order;
       std::vector<std::pair<int, int>> ranges;

@@ -118,6 +118,7 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
 size_t search_args_bytes();
 // dynamic shared memory of one k_search CTA for the given ligand maxima
 size_t search_smem_bytes(int N, int n, int m, int dtot);
+int search_warps_per_cta();
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s);
 // sub-API kernels

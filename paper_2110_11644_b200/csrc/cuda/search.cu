@@ -34,7 +34,10 @@ namespace vsd {
 
 namespace {
 
-constexpr int kWarps = 4;
+#ifndef VS_SEARCH_WARPS
+#define VS_SEARCH_WARPS 2  // warps per CTA: small CTAs pack shared memory tighter (measured)
+#endif
+constexpr int kWarps = VS_SEARCH_WARPS;
 constexpr int kGroup = 16;  // neighbours per group (>= 12)
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
@@ -79,9 +82,9 @@ struct search_args {
   int *work;
   int n_items;
   const int *lig_index;  // bucket launches: item / k -> ligand (NULL: identity)
-  int Nmax, nmax, mmax, dmax;
+  int Nmax, nmax, mmax;
   int warp_doubles;
-  int o_Pd, o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints;
+  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints;
 };
 
 // Offset (in doubles) of variant v's matrix for torsion u >= t(v) inside the
@@ -117,27 +120,6 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
   return true;
 }
 
-// Stage-t positions of the D_t heavy atoms (apply the current torsions < t):
-// the starting points of the torsion-neighbour chains.  Rebuilt whenever the
-// current torsion matrices change.
-__device__ __noinline__ void rebuild_pd(double *Pd, const uint16_t *ditems, const int *doff, const int *dcnt, int m,
-                                        const uint16_t *hl, const double *base, const uint32_t *tm,
-                                        const double *Mcur, int lane) {
-  if (m == 0) return;
-  const int total = doff[m - 1] + dcnt[m - 1];
-  for (int k = lane; k < total; k += 32) {
-    int t = 0;
-    while (k >= doff[t] + dcnt[t]) ++t;
-    const int a = hl[ditems[k]];
-    d3 x = ld3(base + 3 * a);
-    const uint32_t mask = tm[a];
-#pragma unroll 1
-    for (int u = 0; u < t; ++u)
-      if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
-    st3(Pd + 3 * k, x);
-  }
-}
-
 // Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
 // the transformed coordinates to `scratch`, then three lanes run the
 // Eigen-order row sums (dmath.cuh centroid_row).  One out-of-line copy.
@@ -149,7 +131,7 @@ __device__ __noinline__ void compute_pivot(double *scratch, const double *tors, 
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args A) {
   extern __shared__ double sm[];
   double *pal = sm;  // 16 palette values (CTA-wide)
   const int lane = threadIdx.x & 31;
@@ -157,7 +139,6 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
   if (threadIdx.x < 16) pal[threadIdx.x] = MODE == 0 ? 0.0 : A.p.palette[threadIdx.x];
   __syncthreads();
   double *W = sm + 16 + (size_t)warp * A.warp_doubles;
-  double *Pd = W + A.o_Pd;  // stage-t positions of the D_t heavy atoms
   double *tors = W + A.o_tors;
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
@@ -201,7 +182,6 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
     const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
     const int *dcnt = b.d_count + t0, *doff = b.d_off + t0;
     const uint32_t *titems = b.titems + 2 * b.ditem_base[l];
-    const uint16_t *ditems = b.ditems + b.ditem_base[l];
     const int J = 12 + 2 * m;
     unsigned long long evals = 0;
 
@@ -242,7 +222,6 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
         if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
       st3(tors + 3 * a, x);
     }
-    rebuild_pd(Pd, ditems, doff, dcnt, m, hl, base, tm, Mcur, lane);
     // initial_poses entry point: the flat centroid of these angles
     // (search.cpp:89-90) instead of flatten's
     if (!ls_mode && A.ang_in) {
@@ -399,14 +378,14 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
           const uint32_t *ti = titems + 2 * doff[tlo];
           for (int it = lane; it < items; it += 32) {
             const uint32_t e = ti[it];
-            const int h = e & 255, v = (e >> 8) & 63, t = v >> 1;
+            const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
             const int a = hl[h];
-            d3 x = ld3(Pd + 3 * (e >> 14));  // the atom before torsion t
+            d3 x = ld3(base + 3 * a);
             const uint32_t mask = tm[a];
             #pragma unroll 1
-            for (int u = t; u < m; ++u) {
+            for (int u = 0; u < m; ++u) {
               if (!((mask >> u) & 1u)) continue;
-              x = torsion_apply(Mvar + mvar_off(v, u, m), x);
+              x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
             }
             bool out;
             vb[(v - 2 * tlo) * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, x, a), out);
@@ -484,7 +463,6 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
               if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
             st3(tors + 3 * a, x);
           }
-          rebuild_pd(Pd, ditems, doff, dcnt, m, hl, base, tm, Mcur, lane);
         }
         #pragma unroll 1
         for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
@@ -537,10 +515,10 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_search(search_args A) {
 namespace {
 
 struct Layout {
-  int o_Pd, o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints, total;
+  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints, total;
 };
 
-Layout layout(int Nm, int nm, int mm, int dtot) {
+Layout layout(int Nm, int nm, int mm) {
   Layout L{};
   int o = 0;
   auto take = [&](int n) {
@@ -548,7 +526,6 @@ Layout layout(int Nm, int nm, int mm, int dtot) {
     o += (n + 1) & ~1;  // keep 16-byte alignment
     return at;
   };
-  L.o_Pd = take(3 * (dtot > 0 ? dtot : 1));
   L.o_tors = take(3 * Nm);
   L.o_Mcur = take(12 * mm);
   L.o_Mvar = take(12 * mm * (mm + 1));
@@ -567,8 +544,7 @@ Layout layout(int Nm, int nm, int mm, int dtot) {
 }
 
 cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
-  const Layout L = layout(A.Nmax, A.nmax, A.mmax, A.dmax);
-  A.o_Pd = L.o_Pd;
+  const Layout L = layout(A.Nmax, A.nmax, A.mmax);
   A.o_tors = L.o_tors;
   A.o_Mcur = L.o_Mcur;
   A.o_Mvar = L.o_Mvar;
@@ -613,8 +589,11 @@ void set_lattice_table_search(const double *sc72) { cudaMemcpyToSymbol(c_lattice
 
 size_t search_args_bytes() { return sizeof(search_args); }
 
+int search_warps_per_cta() { return kWarps; }
+
 size_t search_smem_bytes(int N, int n, int m, int dtot) {
-  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1, dtot);
+  (void)dtot;
+  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1);
   return (size_t)(16 + L.total * kWarps) * sizeof(double);
 }
 
@@ -622,6 +601,7 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf, const int *lig_index,
                           int n_lig, int dmax) {
+  (void)dmax;
   (void)args_buf;
   search_args A{};
   A.b = b;
@@ -632,7 +612,6 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
   A.o = o;
   A.work = work_counter;
   A.lig_index = lig_index;
-  A.dmax = dmax;
   A.n_items = (lig_index ? n_lig : b.n_lig) * c.k;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
@@ -654,7 +633,6 @@ cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const 
   A.o = o;
   A.ang_in = angles;
   A.work = work_counter;
-  A.dmax = nmax_heavy * mmax;
   A.n_items = b.n_lig * c.k;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
@@ -678,7 +656,6 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
   A.ang_in = ang_in;
   A.conf_in = conf_in;
   A.work = work_counter;
-  A.dmax = nmax_heavy * mmax;
   A.n_items = b.n_lig;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
