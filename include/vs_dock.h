@@ -232,6 +232,14 @@ vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const 
  * device (the roofline denominators of this CUDA-core path). */
 int vs_measure_peaks(int device, double out[3]);
 
+/* Device self-test of the branch-free square root used by the kernels
+ * (dmath.cuh dsqrt) against the IEEE sqrt: n inputs drawn from seed (random
+ * doubles over the whole exponent range, squares of random doubles +- a few
+ * ulps -- the rounding-boundary cases -- and distances in [1e-4, 1e4] A^2).
+ * Writes the number of bitwise mismatches and the first bad input.
+ * Returns 0 on success (test ran), nonzero on a CUDA failure. */
+int vs_selftest_sqrt(int device, uint64_t n, uint64_t seed, uint64_t *mismatches, double *first_bad);
+
 #ifdef __cplusplus
 }
 #endif

@@ -157,6 +157,10 @@ cudaError_t launch_setup(const batch_dev &b, int restarts, cudaStream_t s) {
 // torsions t..m-1 to its private copy (layout [atom][xyz][candidate]) and
 // sums all pair distances sequentially (transform.cpp:83-90).
 constexpr int kFlatThreads = 64;
+#ifndef VS_FLAT_UNROLL
+#define VS_FLAT_UNROLL 4
+#endif
+constexpr int kFlatUnroll = VS_FLAT_UNROLL;  // independent pair distances in flight per thread
 
 __device__ __forceinline__ void lattice_sc(int idx, double &s, double &c) {
   s = c_lattice_sc[2 * idx];
@@ -227,21 +231,19 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
           for (int i = 0; i + 1 < N; ++i) {
             const d3 xi{C[(3 * i) * CB], C[(3 * i + 1) * CB], C[(3 * i + 2) * CB]};
             int j = i + 1;
-            for (; j + 3 < N; j += 4) {
-              double d[4];
+            for (; j + kFlatUnroll - 1 < N; j += kFlatUnroll) {
+              double d[kFlatUnroll];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
+              for (int q = 0; q < kFlatUnroll; ++q) {
                 const d3 xj{C[(3 * (j + q)) * CB], C[(3 * (j + q) + 1) * CB], C[(3 * (j + q) + 2) * CB]};
-                d[q] = sqrt(sqn3(sub3(xi, xj)));
+                d[q] = dsqrt(sqn3(sub3(xi, xj)));
               }
-              sum += d[0];
-              sum += d[1];
-              sum += d[2];
-              sum += d[3];
+#pragma unroll
+              for (int q = 0; q < kFlatUnroll; ++q) sum += d[q];
             }
             for (; j < N; ++j) {
               const d3 xj{C[(3 * j) * CB], C[(3 * j + 1) * CB], C[(3 * j + 2) * CB]};
-              sum += sqrt(sqn3(sub3(xi, xj)));
+              sum += dsqrt(sqn3(sub3(xi, xj)));
             }
           }
           spread[o] = sum;
@@ -348,7 +350,7 @@ __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, dou
   for (int q = lo; q < hi; ++q) {
     const int j = list ? __ldg(list + q) : q;
     const d3 pp{__ldg(p.pxyz + 3 * j), __ldg(p.pxyz + 3 * j + 1), __ldg(p.pxyz + 3 * j + 2)};
-    const double d = sqrt(sqn3(sub3(x, pp)));
+    const double d = dsqrt(sqn3(sub3(x, pp)));
     if (d >= 4.5) continue;
     ++pairs;
     const double ramp = d <= 3.5 ? 1.0 : (4.5 - d) / (4.5 - 3.5);
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
         const int a = hl[h];
         sum += sqn3(sub3(ld3(ci + 3 * a), ld3(cl + 3 * a)));
       }
-      if (sqrt(sum / (double)n) <= c.rmsd_threshold) atomicMin(&first_match, li);
+      if (dsqrt(sum / (double)n) <= c.rmsd_threshold) atomicMin(&first_match, li);
     }
     __syncthreads();
     if (tid == 0) {
@@ -578,7 +580,7 @@ __global__ void __launch_bounds__(kSelThreads) k_cluster(batch_dev b, int np, co
         const int a = hl[h];
         sum += sqn3(sub3(ld3(confs + 3 * ((size_t)idx * N + a)), ld3(confs + 3 * ((size_t)leaders[li] * N + a))));
       }
-      if (sqrt(sum / (double)n) <= threshold) joined = 1;
+      if (dsqrt(sum / (double)n) <= threshold) joined = 1;
     }
     __syncthreads();
     if (tid == 0) {

@@ -6,6 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
+
+#include "dmath.cuh"
 
 namespace {
 
@@ -70,7 +73,61 @@ double rate(F launch, double ops) {
   return 3.0 * ops / (ms * 1e-3);
 }
 
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_sqrt_check(uint64_t n, uint64_t seed, unsigned long long *bad, unsigned long long *first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix64(seed ^ mix64(i));
+    double x;
+    switch (i % 3) {
+      case 0:  // any finite non-negative double (subnormals included)
+        x = __longlong_as_double((long long)(r & 0x7fefffffffffffffull));
+        break;
+      case 1: {  // s^2 +- k ulp: inputs whose sqrt sits next to a rounding midpoint
+        const double s = 1.0 + (double)(r >> 11) * 0x1p-53;  // [1, 2)
+        const int sh = (int)((r >> 3) & 255) - 128;
+        const double sq = __dmul_rn(s, s) * exp2((double)(2 * sh));
+        x = __longlong_as_double(__double_as_longlong(sq) + (long long)(r & 7) - 3);
+        break;
+      }
+      default: {  // squared distances of the dock path
+        x = 1e-4 + (double)(r >> 11) * 0x1p-53 * 1e4;
+        break;
+      }
+    }
+    if (!(x >= 0.0)) continue;
+    const double a = vsd::dsqrt(x), b = sqrt(x);
+    if (__double_as_longlong(a) != __double_as_longlong(b)) {
+      if (atomicAdd(bad, 1ull) == 0) *first = (unsigned long long)__double_as_longlong(x);
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" int vs_selftest_sqrt(int device, uint64_t n, uint64_t seed, uint64_t *mismatches, double *first_bad) {
+  if (cudaSetDevice(device) != cudaSuccess) return 2;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  unsigned long long *buf = nullptr;
+  if (cudaMalloc(&buf, 16) != cudaSuccess) return 3;
+  cudaMemset(buf, 0, 16);
+  k_sqrt_check<<<sms * 8, 256>>>(n, seed, buf, buf + 1);
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpy(h, buf, 16, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (mismatches) *mismatches = h[0];
+  if (first_bad) {
+    long long v = (long long)h[1];
+    std::memcpy(first_bad, &v, sizeof v);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
 
 extern "C" int vs_measure_peaks(int device, double out[3]) {
   if (cudaSetDevice(device) != cudaSuccess) return 2;
