@@ -64,44 +64,62 @@ VS_HD dd dd_add(dd a, dd b) {
 #define VS_SIN_TERMS 15
 #define VS_COS_TERMS 16
 
+#define VS_SIN_TABLE \
+  {0x1.0000000000000p+0, 0x0.0p+0}, \
+  {-0x1.5555555555555p-3, -0x1.5555555555555p-57}, \
+  {0x1.1111111111111p-7, 0x1.1111111111111p-63}, \
+  {-0x1.a01a01a01a01ap-13, -0x1.a01a01a01a01ap-73}, \
+  {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73}, \
+  {-0x1.ae64567f544e4p-26, 0x1.c062e06d1f209p-80}, \
+  {0x1.6124613a86d09p-33, 0x1.f28e0cc748ebep-87}, \
+  {-0x1.ae7f3e733b81fp-41, -0x1.1d8656b0ee8cbp-97}, \
+  {0x1.952c77030ad4ap-49, 0x1.ac981465ddc6cp-103}, \
+  {-0x1.2f49b46814157p-57, -0x1.2650f61dbdcb4p-112}, \
+  {0x1.71b8ef6dcf572p-66, -0x1.d043ae40c4647p-120}, \
+  {-0x1.761b41316381ap-75, 0x1.3423c7d91404fp-130}, \
+  {0x1.3f3ccdd165fa9p-84, -0x1.58ddadf344487p-139}, \
+  {-0x1.d1ab1c2dccea3p-94, -0x1.054d0c78aea14p-149}, \
+  {0x1.259f98b4358adp-103, 0x1.eaf8c39dd9bc5p-157},
+#define VS_COS_TABLE \
+  {0x1.0000000000000p+0, 0x0.0p+0}, \
+  {-0x1.0000000000000p-1, 0x0.0p+0}, \
+  {0x1.5555555555555p-5, 0x1.5555555555555p-59}, \
+  {-0x1.6c16c16c16c17p-10, 0x1.f49f49f49f49fp-65}, \
+  {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76}, \
+  {-0x1.27e4fb7789f5cp-22, -0x1.cbbc05b4fa99ap-76}, \
+  {0x1.1eed8eff8d898p-29, -0x1.2aec959e14c06p-83}, \
+  {-0x1.93974a8c07c9dp-37, -0x1.05d6f8a2efd1fp-92}, \
+  {0x1.ae7f3e733b81fp-45, 0x1.1d8656b0ee8cbp-101}, \
+  {-0x1.6827863b97d97p-53, -0x1.eec01221a8b0bp-107}, \
+  {0x1.e542ba4020225p-62, 0x1.ea72b4afe3c2fp-120}, \
+  {-0x1.0ce396db7f853p-70, 0x1.aebcdbd20331cp-124}, \
+  {0x1.f2cf01972f578p-80, -0x1.9ada5fcc1ab14p-135}, \
+  {-0x1.88e85fc6a4e5ap-89, 0x1.71c37ebd16540p-143}, \
+  {0x1.0a18a2635085dp-98, 0x1.b9e2e28e1aa54p-153}, \
+  {-0x1.3932c5047d60ep-108, -0x1.832b7b530a627p-162},
+
+/* Coefficient tables: constant memory on the device (uniform index, no
+ * branches), plain static arrays on the host; same literals. */
+#if defined(__CUDACC__)
+static __constant__ double vs_sin_tab_d[VS_SIN_TERMS][2] = {VS_SIN_TABLE};
+static __constant__ double vs_cos_tab_d[VS_COS_TERMS][2] = {VS_COS_TABLE};
+#endif
+static const double vs_sin_tab_h[VS_SIN_TERMS][2] = {VS_SIN_TABLE};
+static const double vs_cos_tab_h[VS_COS_TERMS][2] = {VS_COS_TABLE};
+
 VS_HD dd sin_coeff(int n) {
-  switch (n) {
-    case 0: return {0x1.0000000000000p+0, 0x0.0p+0};
-    case 1: return {-0x1.5555555555555p-3, -0x1.5555555555555p-57};
-    case 2: return {0x1.1111111111111p-7, 0x1.1111111111111p-63};
-    case 3: return {-0x1.a01a01a01a01ap-13, -0x1.a01a01a01a01ap-73};
-    case 4: return {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73};
-    case 5: return {-0x1.ae64567f544e4p-26, 0x1.c062e06d1f209p-80};
-    case 6: return {0x1.6124613a86d09p-33, 0x1.f28e0cc748ebep-87};
-    case 7: return {-0x1.ae7f3e733b81fp-41, -0x1.1d8656b0ee8cbp-97};
-    case 8: return {0x1.952c77030ad4ap-49, 0x1.ac981465ddc6cp-103};
-    case 9: return {-0x1.2f49b46814157p-57, -0x1.2650f61dbdcb4p-112};
-    case 10: return {0x1.71b8ef6dcf572p-66, -0x1.d043ae40c4647p-120};
-    case 11: return {-0x1.761b41316381ap-75, 0x1.3423c7d91404fp-130};
-    case 12: return {0x1.3f3ccdd165fa9p-84, -0x1.58ddadf344487p-139};
-    case 13: return {-0x1.d1ab1c2dccea3p-94, -0x1.054d0c78aea14p-149};
-    default: return {0x1.259f98b4358adp-103, 0x1.eaf8c39dd9bc5p-157};
-  }
+#if defined(__CUDA_ARCH__)
+  return {vs_sin_tab_d[n][0], vs_sin_tab_d[n][1]};
+#else
+  return {vs_sin_tab_h[n][0], vs_sin_tab_h[n][1]};
+#endif
 }
 VS_HD dd cos_coeff(int n) {
-  switch (n) {
-    case 0: return {0x1.0000000000000p+0, 0x0.0p+0};
-    case 1: return {-0x1.0000000000000p-1, 0x0.0p+0};
-    case 2: return {0x1.5555555555555p-5, 0x1.5555555555555p-59};
-    case 3: return {-0x1.6c16c16c16c17p-10, 0x1.f49f49f49f49fp-65};
-    case 4: return {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76};
-    case 5: return {-0x1.27e4fb7789f5cp-22, -0x1.cbbc05b4fa99ap-76};
-    case 6: return {0x1.1eed8eff8d898p-29, -0x1.2aec959e14c06p-83};
-    case 7: return {-0x1.93974a8c07c9dp-37, -0x1.05d6f8a2efd1fp-92};
-    case 8: return {0x1.ae7f3e733b81fp-45, 0x1.1d8656b0ee8cbp-101};
-    case 9: return {-0x1.6827863b97d97p-53, -0x1.eec01221a8b0bp-107};
-    case 10: return {0x1.e542ba4020225p-62, 0x1.ea72b4afe3c2fp-120};
-    case 11: return {-0x1.0ce396db7f853p-70, 0x1.aebcdbd20331cp-124};
-    case 12: return {0x1.f2cf01972f578p-80, -0x1.9ada5fcc1ab14p-135};
-    case 13: return {-0x1.88e85fc6a4e5ap-89, 0x1.71c37ebd16540p-143};
-    case 14: return {0x1.0a18a2635085dp-98, 0x1.b9e2e28e1aa54p-153};
-    default: return {-0x1.3932c5047d60ep-108, -0x1.832b7b530a627p-162};
-  }
+#if defined(__CUDA_ARCH__)
+  return {vs_cos_tab_d[n][0], vs_cos_tab_d[n][1]};
+#else
+  return {vs_cos_tab_h[n][0], vs_cos_tab_h[n][1]};
+#endif
 }
 
 /* Correctly rounded sin(x) and cos(x). */
@@ -133,17 +151,18 @@ VS_HD void sincos_cr(double x, double *s_out, double *c_out) {
 
   /* Loops kept rolled: this routine is cold on the device (called only when
    * a torsion angle changes) and must not bloat the search kernel's code. */
+  /* The two Horner recurrences are independent; one loop runs both so their
+   * dependency chains overlap (same operations, same order per polynomial). */
   dd ps = sin_coeff(VS_SIN_TERMS - 1);
+  dd pc = dd_add(dd_mul(cos_coeff(VS_COS_TERMS - 1), r2), cos_coeff(VS_COS_TERMS - 2));
 #if defined(__CUDACC__)
 #pragma unroll 1
 #endif
-  for (int n = VS_SIN_TERMS - 2; n >= 0; --n) ps = dd_add(dd_mul(ps, r2), sin_coeff(n));
+  for (int n = VS_SIN_TERMS - 2; n >= 0; --n) {
+    ps = dd_add(dd_mul(ps, r2), sin_coeff(n));
+    pc = dd_add(dd_mul(pc, r2), cos_coeff(n));
+  }
   const dd sr = dd_mul(ps, r);
-  dd pc = cos_coeff(VS_COS_TERMS - 1);
-#if defined(__CUDACC__)
-#pragma unroll 1
-#endif
-  for (int n = VS_COS_TERMS - 2; n >= 0; --n) pc = dd_add(dd_mul(pc, r2), cos_coeff(n));
 
   /* hi parts are RN(hi + lo) after fast_two_sum normalisation. */
   const double sv = sr.hi;

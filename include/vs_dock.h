@@ -240,6 +240,12 @@ int vs_measure_peaks(int device, double out[3]);
  * Returns 0 on success (test ran), nonzero on a CUDA failure. */
 int vs_selftest_sqrt(int device, uint64_t n, uint64_t seed, uint64_t *mismatches, double *first_bad);
 
+/* Same for the shared-reciprocal division (dmath.cuh drecip/ddiv_r) against
+ * IEEE a / b: random operands over the fast-path range, quotients next to
+ * rounding midpoints, and unit-vector components over norms (signed zeros
+ * included). */
+int vs_selftest_div(int device, uint64_t n, uint64_t seed, uint64_t *mismatches, double *first_bad);
+
 #ifdef __cplusplus
 }
 #endif

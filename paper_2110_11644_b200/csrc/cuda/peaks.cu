@@ -108,7 +108,60 @@ __global__ void k_sqrt_check(uint64_t n, uint64_t seed, unsigned long long *bad,
   }
 }
 
+__global__ void k_div_check(uint64_t n, uint64_t seed, unsigned long long *bad, unsigned long long *first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix64(seed ^ mix64(i)), r2 = mix64(r);
+    double a, b;
+    switch (i % 3) {
+      case 0: {  // random doubles in the fast-path range
+        const long long ea = (long long)((r >> 52) % 800) - 400 + 1023, eb = (long long)((r2 >> 52) % 800) - 400 + 1023;
+        a = __longlong_as_double((long long)((r & 0x800fffffffffffffull) | ((uint64_t)ea << 52)));
+        b = __longlong_as_double((long long)((r2 & 0x800fffffffffffffull) | ((uint64_t)eb << 52)));
+        break;
+      }
+      case 1: {  // a = q * b +- k ulp: quotients next to rounding midpoints
+        const double q = 1.0 + (double)(r >> 11) * 0x1p-53;
+        b = 1.0 + (double)(r2 >> 11) * 0x1p-53;
+        const double qb = __dmul_rn(q, b);
+        a = __longlong_as_double(__double_as_longlong(qb) + (long long)(r2 & 7) - 3);
+        if (r & 1) a = -a;
+        break;
+      }
+      default: {  // the dock path: unit-vector components / norms
+        a = ((double)(r >> 11) * 0x1p-53 - 0.5) * 8.0;
+        b = 1e-3 + (double)(r2 >> 11) * 0x1p-53 * 4.0;
+        if ((r & 15) == 0) a = (r & 16) ? 0.0 : -0.0;
+        break;
+      }
+    }
+    if (!(vsd::drange_ok(a) && vsd::drange_ok(b)) || b == 0.0) continue;
+    const double x = vsd::ddiv_r(a, b, vsd::drecip(b)), y = a / b;
+    if (__double_as_longlong(x) != __double_as_longlong(y)) {
+      if (atomicAdd(bad, 1ull) == 0) *first = (unsigned long long)__double_as_longlong(a);
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" int vs_selftest_div(int device, uint64_t n, uint64_t seed, uint64_t *mismatches, double *first_bad) {
+  if (cudaSetDevice(device) != cudaSuccess) return 2;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  unsigned long long *buf = nullptr;
+  if (cudaMalloc(&buf, 16) != cudaSuccess) return 3;
+  cudaMemset(buf, 0, 16);
+  k_div_check<<<sms * 8, 256>>>(n, seed, buf, buf + 1);
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpy(h, buf, 16, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (mismatches) *mismatches = h[0];
+  if (first_bad) {
+    long long v = (long long)h[1];
+    std::memcpy(first_bad, &v, sizeof v);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
 
 extern "C" int vs_selftest_sqrt(int device, uint64_t n, uint64_t seed, uint64_t *mismatches, double *first_bad) {
   if (cudaSetDevice(device) != cudaSuccess) return 2;

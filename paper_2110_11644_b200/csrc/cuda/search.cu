@@ -38,7 +38,10 @@ namespace {
 #define VS_SEARCH_WARPS 2  // warps per CTA: small CTAs pack shared memory tighter (measured)
 #endif
 constexpr int kWarps = VS_SEARCH_WARPS;
-constexpr int kGroup = 16;  // neighbours per group (>= 12)
+#ifndef VS_SEARCH_GROUP
+#define VS_SEARCH_GROUP 12
+#endif
+constexpr int kGroup = VS_SEARCH_GROUP;  // neighbours per group (>= 12, even; 12 measured best)
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
@@ -52,6 +55,29 @@ __device__ __forceinline__ void st3(double *p, d3 v) {
 __device__ __noinline__ void sincos_cr_dev(double a, double *s, double *c) { vs_crtrig::sincos_cr(a, s, c); }
 
 __constant__ double c_lattice_sc_s[72];
+
+// Development-only phase profile (build with -DVS_PHASE_PROF): per-warp
+// clock64() time spent in each phase of the search, summed over warps.
+#ifdef VS_PHASE_PROF
+__device__ unsigned long long g_phase[16];
+#define PH_DECL                        \
+  unsigned long long ph_t = clock64(); \
+  unsigned long long ph_acc[16] = {0};
+#define PH(k)                                 \
+  {                                           \
+    __syncwarp();                             \
+    const unsigned long long ph_now = clock64(); \
+    ph_acc[k] += ph_now - ph_t;               \
+    ph_t = ph_now;                            \
+  }
+#define PH_FLUSH \
+  if (lane == 0) \
+    for (int i = 0; i < 16; ++i) atomicAdd(&g_phase[i], ph_acc[i]);
+#else
+#define PH_DECL
+#define PH(k)
+#define PH_FLUSH
+#endif
 __device__ __forceinline__ double c_lattice_sc_dev(int i) { return c_lattice_sc_s[i]; }
 
 enum {
@@ -80,10 +106,11 @@ struct search_args {
   const double *ang_in;
   const double *conf_in;
   int *work;
-  int n_items;
-  const int *lig_index;  // bucket launches: item / k -> ligand (NULL: identity)
-  int Nmax, nmax, mmax;
+  int n_lig;             // ligands of this launch (each: k restarts)
+  const int *lig_index;  // bucket launches: launch ligand -> batch ligand (NULL: identity)
+  int Nmax, nmax, mmax, dmax;
   int warp_doubles;
+  int cta_doubles;       // CTA-shared ligand staging (after the palette)
   int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints;
 };
 
@@ -99,14 +126,12 @@ __device__ __forceinline__ int mvar_off(int v, int u, int m) {
 // base coordinates through the current matrices (u' < t) and the new ones
 // (t <= u' < u): the per-atom composition of apply_torsions
 // (transform.cpp:73-81).  Single lane.  out(u) = out + 12 * (u - t).
-__device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, const double *base, const uint16_t *ta,
-                                        const uint16_t *tb, const uint32_t *tm, const double *Mcur,
-                                        const double *sccur, double *out) {
+__device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, const double *ep, const uint32_t *epm,
+                                        const double *Mcur, const double *sccur, double *out) {
   #pragma unroll 1
   for (int u = t; u < m; ++u) {
-    const int a = ta[u], b = tb[u];
-    d3 ea = ld3(base + 3 * a), eb = ld3(base + 3 * b);
-    const uint32_t ma = tm[a], mb = tm[b];
+    d3 ea = ld3(ep + 6 * u), eb = ld3(ep + 6 * u + 3);
+    const uint32_t ma = epm[2 * u], mb = epm[2 * u + 1];
     #pragma unroll 1
     for (int w = 0; w < u; ++w) {
       const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
@@ -118,6 +143,40 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
     if (!torsion_setup(ea, eb, s, c, out + 12 * (u - t))) return false;
   }
   return true;
+}
+
+// Torsion-neighbour matrices of variants vbase + lane (search.cpp:168-176:
+// torsion t = v / 2 moved by +-step), warp-cooperative: all lanes walk the
+// torsions u in the same order, so the endpoint masks (ep/epm: base
+// coordinates and torsion masks of torsion u's bond atoms) and the branches
+// on them are warp-uniform; lane v carries u's endpoints through Mcur
+// (w < t) and through its own new matrices (t <= w < u), then builds matrix
+// u once u >= t -- chain_mats' arithmetic, lanes in lockstep instead of
+// diverging on different chain lengths.  Returns nonzero on a degenerate axis.
+__device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const uint32_t *epm, const double *Mcur,
+                                       const double *sccur, const double *cache, double *Mvar, int lane) {
+  const int v = vbase + lane;
+  const bool act = v < 2 * m;
+  const int t = act ? (v >> 1) : m;
+  double *out = Mvar + (act ? mvar_off(v, t, m) : 0);
+  int bad = 0;
+  #pragma unroll 1
+  for (int u = vbase >> 1; u < m; ++u) {
+    d3 ea = ld3(ep + 6 * u), eb = ld3(ep + 6 * u + 3);
+    const uint32_t ma = epm[2 * u], mb = epm[2 * u + 1];
+    #pragma unroll 1
+    for (int w = 0; w < u; ++w) {
+      const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
+      if ((ma >> w) & 1u) ea = torsion_apply(M, ea);
+      if ((mb >> w) & 1u) eb = torsion_apply(M, eb);
+    }
+    if (u >= t) {
+      const double s = u == t ? cache[2 * v] : sccur[2 * u];
+      const double c = u == t ? cache[2 * v + 1] : sccur[2 * u + 1];
+      if (!torsion_setup(ea, eb, s, c, out + 12 * (u - t))) bad = 1;
+    }
+  }
+  return bad;
 }
 
 // Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
@@ -137,8 +196,19 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x < 16) pal[threadIdx.x] = MODE == 0 ? 0.0 : A.p.palette[threadIdx.x];
-  __syncthreads();
-  double *W = sm + 16 + (size_t)warp * A.warp_doubles;
+  // CTA-shared staging of the current ligand (all warps of the CTA run its
+  // restarts): heavy-atom base coordinates, torsion endpoints, masks, items
+  double *s_bh = sm + 16;                 // 3 * nmax: base coordinates of heavy atom h
+  double *s_ep = s_bh + 3 * A.nmax;       // 6 * mmax: base coordinates of torsion u's endpoints
+  uint32_t *s_tmh = reinterpret_cast<uint32_t *>(s_ep + 6 * A.mmax);  // nmax: torsion mask | parity << 31
+  uint32_t *s_dm = s_tmh + A.nmax;        // nmax: D_t membership of heavy atom h
+  uint32_t *s_hl = s_dm + A.nmax;         // nmax: atom index of heavy atom h
+  uint32_t *s_epm = s_hl + A.nmax;        // 2 * mmax: torsion masks of the endpoints
+  int *s_doff = reinterpret_cast<int *>(s_epm + 2 * A.mmax);  // mmax
+  int *s_dcnt = s_doff + A.mmax;          // mmax
+  uint32_t *s_tit = reinterpret_cast<uint32_t *>(s_dcnt + A.mmax);  // 2 * dmax torsion-neighbour items
+  __shared__ int sh_lig, sh_r;
+  double *W = sm + 16 + A.cta_doubles + (size_t)warp * A.warp_doubles;
   double *tors = W + A.o_tors;
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
@@ -151,8 +221,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   double *ang = W + A.o_ang;
   double *sccur = W + A.o_sccur;
   double *S = W + A.o_state;
-  uint32_t *dm = reinterpret_cast<uint32_t *>(W + A.o_ints);
-  int *cvalid = reinterpret_cast<int *>(dm + A.nmax);
+  int *cvalid = reinterpret_cast<int *>(W + A.o_ints);
 
   const batch_dev &b = A.b;
   const grid_view &g = A.p.g;
@@ -160,35 +229,61 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   const bool ls_mode = A.pose_in != nullptr;
   const int k = ls_mode ? 1 : A.c.k;
   const int nmax = A.nmax;
+  PH_DECL
 
-  while (true) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(A.work, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= A.n_items) break;
-    const int li = item / k, r = item - li * k;
+  while (true) {  // one ligand per CTA pass
+    __syncthreads();  // previous ligand finished by every warp
+    if (threadIdx.x == 0) {
+      sh_lig = atomicAdd(A.work, 1);
+      sh_r = 0;
+    }
+    __syncthreads();
+    const int li = sh_lig;
+    if (li >= A.n_lig) break;
     const int l = A.lig_index ? A.lig_index[li] : li;
-    item = l * k + r;  // global item index of the outputs
     const lig_meta meta = b.meta[l];
     if (meta.status != VS_LIG_OK) {
-      if (lane == 0) A.o.status[item] = meta.status;
+      for (int r = threadIdx.x; r < k; r += blockDim.x) A.o.status[l * k + r] = meta.status;
       continue;
     }
     const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
     const int a0 = b.atom_off[l], t0 = b.tors_off[l];
     const double *base = b.xyz + 3 * (size_t)a0;
-    const uint16_t *hl = b.heavy_list + a0;
     const uint32_t *tm = b.atom_tmask + a0;
-    const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
-    const int *dcnt = b.d_count + t0, *doff = b.d_off + t0;
-    const uint32_t *titems = b.titems + 2 * b.ditem_base[l];
+    {
+      const uint16_t *hl = b.heavy_list + a0;
+      const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
+      const uint32_t *titems = b.titems + 2 * b.ditem_base[l];
+      for (int h = threadIdx.x; h < n; h += blockDim.x) {
+        const int a = hl[h];
+        st3(s_bh + 3 * h, ld3(base + 3 * a));
+        s_tmh[h] = tm[a] | ((uint32_t)(a & 1) << 31);
+        s_dm[h] = b.heavy_dmask[a0 + h];
+        s_hl[h] = (uint32_t)a;
+      }
+      for (int u = threadIdx.x; u < m; u += blockDim.x) {
+        const int ea = ta[u], eb = tb[u];
+        st3(s_ep + 6 * u, ld3(base + 3 * ea));
+        st3(s_ep + 6 * u + 3, ld3(base + 3 * eb));
+        s_epm[2 * u] = tm[ea];
+        s_epm[2 * u + 1] = tm[eb];
+        s_doff[u] = b.d_off[t0 + u];
+        s_dcnt[u] = b.d_count[t0 + u];
+      }
+      for (int i = threadIdx.x; i < 2 * meta.d_total; i += blockDim.x) s_tit[i] = titems[i];
+    }
+    __syncthreads();
     const int J = 12 + 2 * m;
+
+  while (true) {  // restarts of this ligand, one per warp at a time
+    int r = 0;
+    if (lane == 0) r = atomicAdd(&sh_r, 1);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= k) break;
+    const int item = l * k + r;  // global item index of the outputs
     unsigned long long evals = 0;
 
-    // ---- per-ligand tables
-    for (int h = lane; h < n; h += 32) {
-      dm[h] = b.heavy_dmask[a0 + h];
-    }
+    // ---- per-restart tables
     for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
     if (A.ang_in) {  // local_search / initial_poses entry points: arbitrary angles
       for (int u = lane; u < m; u += 32) {
@@ -205,7 +300,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     }
     if (lane == 0) S[S_ERR] = 0.0;
     __syncwarp();
-    if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, base, ta, tb, tm, Mcur, sccur, Mcur))
+    if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, s_ep, s_epm, Mcur, sccur, Mcur))
       S[S_ERR] = 1.0;
     __syncwarp();
     if (S[S_ERR] != 0.0) {
@@ -261,7 +356,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     }
     __syncwarp();
     for (int h = lane; h < n; h += 32) {
-      const int a = hl[h];
+      const int a = s_hl[h];
       bool out;
       vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a), out);
     }
@@ -285,6 +380,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       compute_pivot(vb, tors, S, N, lane);
     }
 
+    PH(0)
     // ---- local_search (search.cpp:121-191)
     int level = 0, n_iter = 0, n_adopt = 0;
     bool failed = false, mvar_valid = false, moved = false;
@@ -292,47 +388,84 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       const double step_t = S[S_STEPT], step_q = S[S_STEPQ];
       // rigid neighbour transforms (lanes 0-11) and, when stale, the
       // torsion-neighbour matrices (lanes 12..; one lane per neighbour)
-      for (int w = lane; w < (mvar_valid ? 12 : J); w += 32) {
-        if (w < 12) {
-          double *X = Rj + 16 * w;
-          if (w < 6) {  // translations (search.cpp:152-158)
-            const int axis = w >> 1;
-            const double sign = (w & 1) ? -1.0 : 1.0;
-            for (int q = 0; q < 9; ++q) X[q] = S[S_R + q];
-            for (int q = 0; q < 3; ++q) X[9 + q] = S[S_T + q];
-            X[9 + axis] = S[S_T + axis] + sign * step_t;
-            for (int q = 0; q < 4; ++q) X[12 + q] = S[S_Q + q];
-          } else {  // rotations about the pivot (search.cpp:159-167)
-            const double *sq = A.c.spin + 4 * (6 * level + (w - 6));
-            const quat spin{sq[0], sq[1], sq[2], sq[3]};
-            const d3 piv = ld3(S + S_PIV);
-            const d3 spin_t = sub3(piv, quat_rotate(spin, piv));
-            const quat cur{S[S_Q], S[S_Q + 1], S[S_Q + 2], S[S_Q + 3]};
-            const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
-            const d3 tt = add3(quat_rotate(spin, ld3(S + S_T)), spin_t);
-            quat_matrix(qn, X);
-            X[9] = tt.x;
-            X[10] = tt.y;
-            X[11] = tt.z;
-            X[12] = qn.x;
-            X[13] = qn.y;
-            X[14] = qn.z;
-            X[15] = qn.w;
-          }
-        } else {  // torsion neighbour matrices (search.cpp:168-176)
-          const int v = w - 12, t = v >> 1;
-          const double sign = (v & 1) ? -1.0 : 1.0;
-          if (!cvalid[v]) {
-            sincos_cr_dev(ang[t] + sign * step_q, &cache[2 * v], &cache[2 * v + 1]);
-            cvalid[v] = 1;
-          }
-          if (!chain_mats(t, cache[2 * v], cache[2 * v + 1], m, base, ta, tb, tm, Mcur, sccur,
-                          Mvar + mvar_off(v, t, m)))
-            S[S_ERR] = 1.0;
+#ifdef VS_PHASE_PROF
+      const bool ph_rebuild = !mvar_valid;
+#endif
+#ifdef VS_PHASE_PROF
+      unsigned int pr_sc = 0, pr_ch = 0, pr_rg = 0;
+      unsigned long long pr0 = clock64();
+#endif
+      // rigid neighbour transforms (lanes 0-11)
+      if (lane < 12) {
+        double *X = Rj + 16 * lane;
+        if (lane < 6) {  // translations (search.cpp:152-158)
+          const int axis = lane >> 1;
+          const double sign = (lane & 1) ? -1.0 : 1.0;
+          for (int q = 0; q < 9; ++q) X[q] = S[S_R + q];
+          for (int q = 0; q < 3; ++q) X[9 + q] = S[S_T + q];
+          X[9 + axis] = S[S_T + axis] + sign * step_t;
+          for (int q = 0; q < 4; ++q) X[12 + q] = S[S_Q + q];
+        } else {  // rotations about the pivot (search.cpp:159-167)
+          const double *sq = A.c.spin + 4 * (6 * level + (lane - 6));
+          const quat spin{sq[0], sq[1], sq[2], sq[3]};
+          const d3 piv = ld3(S + S_PIV);
+          const d3 spin_t = sub3(piv, quat_rotate(spin, piv));
+          const quat cur{S[S_Q], S[S_Q + 1], S[S_Q + 2], S[S_Q + 3]};
+          const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
+          const d3 tt = add3(quat_rotate(spin, ld3(S + S_T)), spin_t);
+          quat_matrix(qn, X);
+          X[9] = tt.x;
+          X[10] = tt.y;
+          X[11] = tt.z;
+          X[12] = qn.x;
+          X[13] = qn.y;
+          X[14] = qn.z;
+          X[15] = qn.w;
         }
       }
+#ifdef VS_PHASE_PROF
+      __syncwarp();
+      pr_rg = (unsigned int)(clock64() - pr0);
+      pr0 = clock64();
+#endif
+      // torsion-neighbour matrices when stale (after a torsion move or a
+      // step halving): sin/cos of the moved angles, then the chains
+      if (!mvar_valid) {
+        #pragma unroll 1
+        for (int vb0 = 0; vb0 < 2 * m; vb0 += 32) {
+          const int v = vb0 + lane;
+          if (v < 2 * m && !cvalid[v]) {
+            const double sign = (v & 1) ? -1.0 : 1.0;
+            sincos_cr_dev(ang[v >> 1] + sign * step_q, &cache[2 * v], &cache[2 * v + 1]);
+            cvalid[v] = 1;
+          }
+          __syncwarp();
+#ifdef VS_PHASE_PROF
+          pr_sc += (unsigned int)(clock64() - pr0);
+          pr0 = clock64();
+#endif
+          if (chain_warp(vb0, m, s_ep, s_epm, Mcur, sccur, cache, Mvar, lane)) S[S_ERR] = 1.0;
+#ifdef VS_PHASE_PROF
+          __syncwarp();
+          pr_ch += (unsigned int)(clock64() - pr0);
+          pr0 = clock64();
+#endif
+        }
+      }
+#ifdef VS_PHASE_PROF
+      if (ph_rebuild) {
+        ph_acc[12] += pr_sc;
+        ph_acc[13] += pr_ch;
+        ph_acc[14] += pr_rg;
+      }
+#endif
       mvar_valid = true;
       __syncwarp();
+      PH(ph_rebuild ? 9 : 1)
+#ifdef VS_PHASE_PROF
+      ph_acc[10] += ph_rebuild ? 1 : 0;
+      ph_acc[11] += 1;
+#endif
       if (S[S_ERR] != 0.0) {
         failed = true;
         break;
@@ -353,7 +486,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           tg = thi;
           j0 = 12 + 2 * tlo;
           jn = 2 * (thi - tlo);
-          items = 2 * (doff[thi - 1] + dcnt[thi - 1] - doff[tlo]);
+          items = 2 * (s_doff[thi - 1] + s_dcnt[thi - 1] - s_doff[tlo]);
         }
         // Two items per lane per step (independent gathers in flight); the
         // rigid and the torsion neighbours run in separate compact loops.
@@ -365,7 +498,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           // rigid neighbours: lane = heavy atom, loop over the 12 transforms
           // (their matrices are warp-uniform shared-memory broadcasts)
           for (int h = lane; h < n; h += 32) {
-            const int a = hl[h];
+            const int a = s_hl[h];
             const d3 x = ld3(tors + 3 * a);
             #pragma unroll 1
             for (int j = 0; j < 12; ++j) {
@@ -375,23 +508,24 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             }
           }
         } else {
-          const uint32_t *ti = titems + 2 * doff[tlo];
+          const uint32_t *ti = s_tit + 2 * s_doff[tlo];
           for (int it = lane; it < items; it += 32) {
             const uint32_t e = ti[it];
             const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
-            const int a = hl[h];
-            d3 x = ld3(base + 3 * a);
-            const uint32_t mask = tm[a];
+            d3 x = ld3(s_bh + 3 * h);
+            const uint32_t mask = s_tmh[h];
             #pragma unroll 1
             for (int u = 0; u < m; ++u) {
               if (!((mask >> u) & 1u)) continue;
               x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
             }
             bool out;
-            vb[(v - 2 * tlo) * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, x, a), out);
+            vb[(v - 2 * tlo) * nmax + h] =
+                field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, x, (int)(mask >> 31)), out);
           }
         }
         __syncwarp();
+        PH(grp == 0 ? 2 : 3)
         // geo_score of each neighbour in the group (grid.cpp:97-101)
         if (lane < jn) {
           const double *row = vb + lane * nmax;
@@ -402,7 +536,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           } else {
             const int t = tlo + (lane >> 1);
             #pragma unroll 4
-            for (int h = 0; h < n; ++h) acc += ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
+            for (int h = 0; h < n; ++h) acc += ((s_dm[h] >> t) & 1u) ? row[h] : vcur[h];
           }
           scores[lane] = acc;
         }
@@ -426,10 +560,11 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             for (int h = lane; h < n; h += 32) vbest[h] = row[h];
           } else {
             const int t = tlo + (gj >> 1);
-            for (int h = lane; h < n; h += 32) vbest[h] = ((dm[h] >> t) & 1u) ? row[h] : vcur[h];
+            for (int h = lane; h < n; h += 32) vbest[h] = ((s_dm[h] >> t) & 1u) ? row[h] : vcur[h];
           }
         }
         __syncwarp();
+        PH(4)
       }
       evals += (unsigned long long)n * J;
       ++n_iter;
@@ -470,6 +605,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         __syncwarp();
         // new pivot = centroid of the adopted conformation (vb is free here)
         compute_pivot(vb, tors, S, N, lane);
+        PH(bj < 12 ? 5 : 6)
       } else {
         if (lane == 0) {
           S[S_STEPT] = S[S_STEPT] * 0.5;
@@ -479,6 +615,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
         mvar_valid = false;
         ++level;
+        PH(7)
       }
       __syncwarp();
     }
@@ -509,17 +646,23 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       if (A.o.adopts) A.o.adopts[item] = n_adopt;
     }
     __syncwarp();
-  }
+    PH(8)
+  }  // restarts
+  }  // ligands
+  PH_FLUSH
 }
 
 namespace {
 
 struct Layout {
   int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints, total;
+  int cta;  // CTA-shared ligand staging, doubles
 };
 
-Layout layout(int Nm, int nm, int mm) {
+Layout layout(int Nm, int nm, int mm, int dm) {
   Layout L{};
+  L.cta = 3 * nm + 6 * mm + (3 * nm + 4 * mm + 2 * dm + 1) / 2 + 1;
+  L.cta = (L.cta + 1) & ~1;
   int o = 0;
   auto take = [&](int n) {
     const int at = o;
@@ -538,13 +681,14 @@ Layout layout(int Nm, int nm, int mm) {
   L.o_ang = take(mm);
   L.o_sccur = take(2 * mm);
   L.o_state = take(S_N);
-  L.o_ints = take((nm + 2 * mm + 3) / 2 + 1);
+  L.o_ints = take((2 * mm + 1) / 2 + 1);
   L.total = o;
   return L;
 }
 
 cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
-  const Layout L = layout(A.Nmax, A.nmax, A.mmax);
+  const Layout L = layout(A.Nmax, A.nmax, A.mmax, A.dmax);
+  A.cta_doubles = L.cta;
   A.o_tors = L.o_tors;
   A.o_Mcur = L.o_Mcur;
   A.o_Mvar = L.o_Mvar;
@@ -560,7 +704,7 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   A.o_ints = L.o_ints;
   A.warp_doubles = L.total;
   const int o = L.total;
-  const size_t smem = (size_t)(16 + o * kWarps) * sizeof(double);
+  const size_t smem = (size_t)(16 + L.cta + o * kWarps) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const void *fn = A.pg.mode == 1 ? (const void *)k_search<1>
                                   : (A.pg.mode == 2 ? (const void *)k_search<2> : (const void *)k_search<0>);
@@ -570,8 +714,7 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
   int blocks = num_sms * per_sm;
-  const int need = (A.n_items + kWarps - 1) / kWarps;
-  if (blocks > need) blocks = need;
+  if (blocks > A.n_lig) blocks = A.n_lig;
   if (blocks < 1) blocks = 1;
   if (A.pg.mode == 1)
     k_search<1><<<blocks, 32 * kWarps, smem, s>>>(A);
@@ -587,21 +730,30 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
 
 void set_lattice_table_search(const double *sc72) { cudaMemcpyToSymbol(c_lattice_sc_s, sc72, sizeof(double) * 72); }
 
+#ifdef VS_PHASE_PROF
+extern "C" int vs_debug_phase_read(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase, z, sizeof z);
+  }
+  return 0;
+}
+#endif
+
 size_t search_args_bytes() { return sizeof(search_args); }
 
 int search_warps_per_cta() { return kWarps; }
 
 size_t search_smem_bytes(int N, int n, int m, int dtot) {
-  (void)dtot;
-  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1);
-  return (size_t)(16 + L.total * kWarps) * sizeof(double);
+  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1, dtot > 0 ? dtot : 1);
+  return (size_t)(16 + L.cta + L.total * kWarps) * sizeof(double);
 }
 
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf, const int *lig_index,
                           int n_lig, int dmax) {
-  (void)dmax;
   (void)args_buf;
   search_args A{};
   A.b = b;
@@ -612,11 +764,12 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
   A.o = o;
   A.work = work_counter;
   A.lig_index = lig_index;
-  A.n_items = (lig_index ? n_lig : b.n_lig) * c.k;
+  A.n_lig = lig_index ? n_lig : b.n_lig;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
-  if (A.n_items == 0) return cudaSuccess;
+  A.dmax = dmax > 0 ? dmax : A.nmax * A.mmax;
+  if (A.n_lig == 0) return cudaSuccess;
   return run_search(A, num_sms, s, launches);
 }
 
@@ -633,11 +786,12 @@ cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const 
   A.o = o;
   A.ang_in = angles;
   A.work = work_counter;
-  A.n_items = b.n_lig * c.k;
+  A.n_lig = b.n_lig;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
-  if (A.n_items == 0) return cudaSuccess;
+  A.dmax = A.nmax * A.mmax;  // upper bound of sum_t |D_t|
+  if (A.n_lig == 0) return cudaSuccess;
   return run_search(A, num_sms, s, nullptr);
 }
 
@@ -656,11 +810,12 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
   A.ang_in = ang_in;
   A.conf_in = conf_in;
   A.work = work_counter;
-  A.n_items = b.n_lig;
+  A.n_lig = b.n_lig;
   A.Nmax = nmax_atoms > 0 ? nmax_atoms : 1;
   A.nmax = nmax_heavy > 0 ? nmax_heavy : 1;
   A.mmax = mmax > 0 ? mmax : 1;
-  if (A.n_items == 0) return cudaSuccess;
+  A.dmax = A.nmax * A.mmax;  // upper bound of sum_t |D_t|
+  if (A.n_lig == 0) return cudaSuccess;
   return run_search(A, num_sms, s, nullptr);
 }
 

@@ -52,6 +52,7 @@ SIGNATURES = {
     "vs_local_search_batch": (C.c_int, [_vp, _vp, _LB, _CF, _PO, _d, _d, _u64, _i32]),
     "vs_measure_peaks": (C.c_int, [C.c_int, _d]),
     "vs_selftest_sqrt": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), _d]),
+    "vs_selftest_div": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), _d]),
     # vs_prep.h
     "vs_prep_smiles_batch": (C.c_int, [C.c_int32, C.POINTER(C.c_char_p), C.c_int32, C.c_int32, C.POINTER(_vp)]),
     "vs_ligand_set_view": (C.c_int, [_vp, _LB, C.POINTER(_i32)]),

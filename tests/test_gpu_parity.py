@@ -41,6 +41,18 @@ def test_branch_free_sqrt_is_ieee(gpu_ctx):
     assert bad.value == 0, f"first mismatch at x={first.value!r}"
 
 
+def test_shared_reciprocal_division_is_ieee(gpu_ctx):
+    """dmath.cuh drecip/ddiv_r (normalisations in torsion_setup and
+    quat_normalized) are bit-identical to IEEE a / b on 3e8 operand pairs."""
+    import ctypes as C
+    from paper_2110_11644_b200 import native
+    bad = C.c_uint64(0)
+    first = C.c_double(0.0)
+    rc = native.lib().vs_selftest_div(0, 300_000_000, 20260819, C.byref(bad), C.byref(first))
+    assert rc == 0
+    assert bad.value == 0, f"first mismatch at a={first.value!r}"
+
+
 def test_trilinear_kats_gpu(gpu_ctx):
     cube = explicit_pocket((2, 2, 2), 1.0, [1, 2, 3, 4, 5, 6, 7, 8])
     v = api.pocket_field_value(cube, [[1, 0, 0], [0, 1, 1], [0.25, 0.5, 0.75], [1, 1, 1], [0.5, 0.5, 1.5],
