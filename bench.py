@@ -312,16 +312,12 @@ def main():
     status = last.results["status"]
     ok = int((status == 0).sum())
 
-    # host top-K merge (merge.cpp:131-135: score desc, SMILES asc) of the last step
+    # host top-K merge of the last step (ranking.py: merge.cpp:131-135 order,
+    # printed 4-decimal score desc, SMILES asc); only K rows per rank travel
+    from paper_2110_11644_b200 import ranking
     K = 1000
-    order = np.lexsort((np.array(smi), -last.results["best_score"]))[:K]
-    top_local = [(float(last.results["best_score"][i]), smi[i]) for i in order]
-    if dist is not None:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, top_local)
-        merged = sorted([x for g in gathered for x in g], key=lambda x: (-x[0], x[1]))[:K]
-    else:
-        merged = top_local
+    top_local = ranking.top_k(last.results["best_score"], smi, K, last.results["status"])
+    merged = ranking.distributed_top_k(top_local, K) if dist is not None else top_local
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -349,7 +345,7 @@ def main():
                    "pocket": "build_pocket(r=12 A, h=0.375 A) -> 65^3, synthetic protein seed 20260819",
                    "l2": "flushed between timed steps (256 MB device write)", "parallelism": f"replica x{world}",
                    "setup_s": round(setup_s, 2)},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world},
         "gpu_launches": launches,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
