@@ -27,7 +27,6 @@ namespace vsd {
 // (search.cpp:33,40), computed on the host with vs_crtrig.
 __constant__ double c_lattice_sc[72];
 constexpr double kPi = 3.14159265358979323846;
-constexpr double kLatticeStep = 2.0 * kPi / 36;
 
 void set_lattice_table(const double *sc72) {
   cudaMemcpyToSymbol(c_lattice_sc, sc72, sizeof(double) * 72);

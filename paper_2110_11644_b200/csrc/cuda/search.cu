@@ -42,6 +42,10 @@ constexpr int kWarps = VS_SEARCH_WARPS;
 #define VS_SEARCH_GROUP 12
 #endif
 constexpr int kGroup = VS_SEARCH_GROUP;  // neighbours per group (>= 12, even; 12 measured best)
+#ifndef VS_RIGID_UNROLL
+#define VS_RIGID_UNROLL 1
+#endif
+constexpr int kRigidUnroll = VS_RIGID_UNROLL;  // rigid samples in flight per lane
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
@@ -50,6 +54,28 @@ __device__ __forceinline__ void st3(double *p, d3 v) {
   p[0] = v.x;
   p[1] = v.y;
   p[2] = v.z;
+}
+
+// 12-double blocks (rotation + translation / pivot) at 16-byte aligned
+// shared-memory addresses, read with 128-bit loads.
+__device__ __forceinline__ void ld12a(const double *p, double r[12]) {
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+  #pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double2 v = q[i];
+    r[2 * i] = v.x;
+    r[2 * i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ d3 torsion_apply_a(const double *m, d3 x) {
+  double r[12];
+  ld12a(m, r);
+  return torsion_apply(r, x);
+}
+__device__ __forceinline__ d3 rigid_col_a(const double *rt, d3 v, int col) {
+  double r[12];
+  ld12a(rt, r);
+  return rigid_col(r, r + 9, v, col);
 }
 
 __device__ __noinline__ void sincos_cr_dev(double a, double *s, double *c) { vs_crtrig::sincos_cr(a, s, c); }
@@ -82,8 +108,8 @@ __device__ __forceinline__ double c_lattice_sc_dev(int i) { return c_lattice_sc_
 
 enum {
   S_Q = 0,      // current rotation (x, y, z, w)
-  S_T = 4,      // current translation
-  S_R = 7,      // current rotation matrix
+  S_R = 4,      // current rotation matrix (16-byte aligned, translation follows:
+  S_T = 13,     //   R and t load as one 12-double block, like the Rj rows)
   S_PIV = 16,   // pivot
   S_GEO = 19,   // current geo_score
   S_STEPT = 20,
@@ -135,8 +161,8 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
     #pragma unroll 1
     for (int w = 0; w < u; ++w) {
       const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
-      if ((ma >> w) & 1u) ea = torsion_apply(M, ea);
-      if ((mb >> w) & 1u) eb = torsion_apply(M, eb);
+      if ((ma >> w) & 1u) ea = torsion_apply_a(M, ea);
+      if ((mb >> w) & 1u) eb = torsion_apply_a(M, eb);
     }
     const double s = u == t ? st : sccur[2 * u];
     const double c = u == t ? ct : sccur[2 * u + 1];
@@ -165,10 +191,11 @@ __device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const
     d3 ea = ld3(ep + 6 * u), eb = ld3(ep + 6 * u + 3);
     const uint32_t ma = epm[2 * u], mb = epm[2 * u + 1];
     #pragma unroll 1
-    for (int w = 0; w < u; ++w) {
+    for (uint32_t bb = (ma | mb) & ((1u << u) - 1u); bb; bb &= bb - 1u) {
+      const int w = __ffs(bb) - 1;
       const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
-      if ((ma >> w) & 1u) ea = torsion_apply(M, ea);
-      if ((mb >> w) & 1u) eb = torsion_apply(M, eb);
+      if ((ma >> w) & 1u) ea = torsion_apply_a(M, ea);
+      if ((mb >> w) & 1u) eb = torsion_apply_a(M, eb);
     }
     if (u >= t) {
       const double s = u == t ? cache[2 * v] : sccur[2 * u];
@@ -183,7 +210,7 @@ __device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const
 // the transformed coordinates to `scratch`, then three lanes run the
 // Eigen-order row sums (dmath.cuh centroid_row).  One out-of-line copy.
 __device__ __noinline__ void compute_pivot(double *scratch, const double *tors, double *S, int N, int lane) {
-  for (int a = lane; a < N; a += 32) st3(scratch + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
+  for (int a = lane; a < N; a += 32) st3(scratch + 3 * a, rigid_col_a(S + S_R, ld3(tors + 3 * a), a));
   __syncwarp();
   if (lane < 3) S[S_PIV + lane] = centroid_row(scratch, N, lane);
   __syncwarp();
@@ -191,7 +218,7 @@ __device__ __noinline__ void compute_pivot(double *scratch, const double *tors, 
 
 template <int MODE>
 __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args A) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double *pal = sm;  // 16 palette values (CTA-wide)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -313,8 +340,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       d3 x = ld3(base + 3 * a);
       const uint32_t mask = tm[a];
       #pragma unroll 1
-      for (int u = 0; u < m; ++u)
-        if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
+      for (uint32_t bb = mask; bb; bb &= bb - 1u) x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
       st3(tors + 3 * a, x);
     }
     // initial_poses entry point: the flat centroid of these angles
@@ -358,7 +384,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     for (int h = lane; h < n; h += 32) {
       const int a = s_hl[h];
       bool out;
-      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a), out);
+      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, ld3(tors + 3 * a), a), out);
     }
     __syncwarp();
     if (lane == 0) {
@@ -500,11 +526,11 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           for (int h = lane; h < n; h += 32) {
             const int a = s_hl[h];
             const d3 x = ld3(tors + 3 * a);
-            #pragma unroll 1
+            #pragma unroll kRigidUnroll
             for (int j = 0; j < 12; ++j) {
               const double *X = Rj + 16 * j;
               bool out;
-              vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col(X, X + 9, x, a), out);
+              vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(X, x, a), out);
             }
           }
         } else {
@@ -514,14 +540,15 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
             d3 x = ld3(s_bh + 3 * h);
             const uint32_t mask = s_tmh[h];
+            const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
             #pragma unroll 1
-            for (int u = 0; u < m; ++u) {
-              if (!((mask >> u) & 1u)) continue;
-              x = torsion_apply(u < t ? Mcur + 12 * u : Mvar + mvar_off(v, u, m), x);
+            for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
+              const int u = __ffs(bb) - 1;
+              x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
             }
             bool out;
             vb[(v - 2 * tlo) * nmax + h] =
-                field_value_fast<MODE>(g, pg, pal, rigid_col(S + S_R, S + S_T, x, (int)(mask >> 31)), out);
+                field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x, (int)(mask >> 31)), out);
           }
         }
         __syncwarp();
@@ -594,8 +621,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             d3 x = ld3(base + 3 * a);
             const uint32_t mask = tm[a];
             #pragma unroll 1
-            for (int u = 0; u < m; ++u)
-              if ((mask >> u) & 1u) x = torsion_apply(Mcur + 12 * u, x);
+            for (uint32_t bb = mask; bb; bb &= bb - 1u) x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
             st3(tors + 3 * a, x);
           }
         }
@@ -630,7 +656,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
     } else {
       for (int a = lane; a < N; a += 32)
-        st3(A.o.conf + ck + 3 * a, rigid_col(S + S_R, S + S_T, ld3(tors + 3 * a), a));
+        st3(A.o.conf + ck + 3 * a, rigid_col_a(S + S_R, ld3(tors + 3 * a), a));
     }
     const size_t tk = (size_t)t0 * k + (size_t)r * m;
     for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = ang[u];
