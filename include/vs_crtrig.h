@@ -122,16 +122,38 @@ VS_HD dd cos_coeff(int n) {
 #endif
 }
 
-/* Correctly rounded sin(x) and cos(x). */
-VS_HD void sincos_cr(double x, double *s_out, double *c_out) {
+VS_HD dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+
+/* Taylor series of sin(r), cos(r) in double-double, |r| <= pi/4.  Loops
+ * kept rolled: this routine is cold on the device and must not bloat the
+ * search kernel's code.  The two Horner recurrences are independent; one loop
+ * runs both so their dependency chains overlap (same operations, same order
+ * per polynomial). */
+VS_HD void sincos_poly(dd r, dd r2, dd *s_out, dd *c_out) {
+  dd ps = sin_coeff(VS_SIN_TERMS - 1);
+  dd pc = dd_add(dd_mul(cos_coeff(VS_COS_TERMS - 1), r2), cos_coeff(VS_COS_TERMS - 2));
+#if defined(__CUDACC__)
+#pragma unroll 1
+#endif
+  for (int n = VS_SIN_TERMS - 2; n >= 0; --n) {
+    ps = dd_add(dd_mul(ps, r2), sin_coeff(n));
+    pc = dd_add(dd_mul(pc, r2), cos_coeff(n));
+  }
+  *s_out = dd_mul(ps, r);
+  *c_out = pc;
+}
+
+/* sin(x) and cos(x) as normalised double-double (relative error < 2^-100);
+ * the hi parts are the correctly rounded values. */
+VS_HD void sincos_dd(double x, dd *s_out, dd *c_out) {
   if (x == 0.0) {  /* keeps the sign of zero, as sin does */
-    *s_out = x;
-    *c_out = 1.0;
+    *s_out = dd{x, 0.0};
+    *c_out = dd{1.0, 0.0};
     return;
   }
   if (!(x - x == 0.0)) {  /* inf or nan */
-    *s_out = x - x;
-    *c_out = x - x;
+    *s_out = dd{x - x, 0.0};
+    *c_out = dd{x - x, 0.0};
     return;
   }
   /* k = nearest integer to x*2/pi; r = x - k*pi/2 in double-double.
@@ -149,29 +171,60 @@ VS_HD void sincos_cr(double x, double *s_out, double *c_out) {
   r = dd_add(r, dd{-(kd * P3t), 0.0});
   const dd r2 = dd_mul(r, r);
 
-  /* Loops kept rolled: this routine is cold on the device (called only when
-   * a torsion angle changes) and must not bloat the search kernel's code. */
-  /* The two Horner recurrences are independent; one loop runs both so their
-   * dependency chains overlap (same operations, same order per polynomial). */
-  dd ps = sin_coeff(VS_SIN_TERMS - 1);
-  dd pc = dd_add(dd_mul(cos_coeff(VS_COS_TERMS - 1), r2), cos_coeff(VS_COS_TERMS - 2));
-#if defined(__CUDACC__)
-#pragma unroll 1
-#endif
-  for (int n = VS_SIN_TERMS - 2; n >= 0; --n) {
-    ps = dd_add(dd_mul(ps, r2), sin_coeff(n));
-    pc = dd_add(dd_mul(pc, r2), cos_coeff(n));
+  dd sr, pc;
+  if (fabs(r.hi) < 0x1p-30) {
+    /* tiny reduced argument (x next to a multiple of pi/2, as sums of
+     * lattice angles and torsion steps often are): the next Taylor terms are
+     * below 2^-120 relative */
+    sr = dd_add(r, dd_neg(dd_mul(dd_mul(r2, r), dd{0x1.5555555555555p-3, 0x1.5555555555555p-57})));
+    pc = dd_add(dd{1.0, 0.0}, dd{-0.5 * r2.hi, -0.5 * r2.lo});
+  } else {
+    sincos_poly(r, r2, &sr, &pc);
   }
-  const dd sr = dd_mul(ps, r);
-
-  /* hi parts are RN(hi + lo) after fast_two_sum normalisation. */
-  const double sv = sr.hi;
-  const double cv = pc.hi;
   const long long q = ((long long)kd) & 3;
-  if (q == 0) { *s_out = sv; *c_out = cv; }
-  else if (q == 1) { *s_out = cv; *c_out = -sv; }
-  else if (q == 2) { *s_out = -sv; *c_out = -cv; }
-  else { *s_out = -cv; *c_out = sv; }
+  if (q == 0) { *s_out = sr; *c_out = pc; }
+  else if (q == 1) { *s_out = pc; *c_out = dd_neg(sr); }
+  else if (q == 2) { *s_out = dd_neg(sr); *c_out = dd_neg(pc); }
+  else { *s_out = dd_neg(pc); *c_out = sr; }
+}
+
+/* Correctly rounded sin(x) and cos(x): hi parts of sincos_dd (fast_two_sum
+ * normalisation makes hi = RN(hi + lo)). */
+VS_HD void sincos_cr(double x, double *s_out, double *c_out) {
+  dd s, c;
+  sincos_dd(x, &s, &c);
+  *s_out = s.hi;
+  *c_out = c.hi;
+}
+
+/* The search's torsion moves: a' = RN(a + d) and sin/cos(a') as double-
+ * double from the double-double sin/cos of a and of d (angle addition, then
+ * the exact rounding offset delta = a' - (a + d) to second order).  Relative
+ * error ~2^-103 per call (it accumulates slowly along a chain of moves), so
+ * the hi parts are the correctly rounded sin/cos of a' except within that
+ * distance of a rounding midpoint; tests/test_crtrig.py checks the hi parts
+ * against sincos_cr along random move chains.  Returns false when sin or
+ * cos of a' is below 2^-8 in magnitude (cancellation): then the caller
+ * evaluates sincos_dd(*a_out). */
+VS_HD bool sincos_shift(double a, dd sa, dd ca, double d, dd sd, dd cd, double *a_out, dd *s_out, dd *c_out) {
+  const dd sum = two_sum(a, d); /* a + d = sum.hi + sum.lo exactly */
+  const double del = -sum.lo;   /* a' = (a + d) + del */
+  const dd ss = dd_add(dd_mul(sa, cd), dd_mul(ca, sd));         /* sin(a + d) */
+  const dd cs = dd_add(dd_mul(ca, cd), dd_neg(dd_mul(sa, sd))); /* cos(a + d) */
+  const double h = 0.5 * (del * del);
+  /* sin(a') = ss + cs*del - h*ss ; cos(a') = cs - ss*del - h*cs */
+  const dd sp = two_prod(cs.hi, del);
+  const dd cp = two_prod(ss.hi, del);
+  dd sn = dd_add(ss, sp);
+  sn = dd_add(sn, dd{cs.lo * del - h * ss.hi, 0.0});
+  dd cn = dd_add(cs, dd_neg(cp));
+  cn = dd_add(cn, dd{-(ss.lo * del) - h * cs.hi, 0.0});
+  *a_out = sum.hi;
+  *s_out = sn;
+  *c_out = cn;
+  /* next to a zero of sin or cos the angle addition cancels: the caller
+   * must use sincos_dd(*a_out) instead */
+  return !(fabs(sn.hi) < 0x1p-8 || fabs(cn.hi) < 0x1p-8);
 }
 
 }  // namespace vs_crtrig

@@ -108,6 +108,14 @@ class Oracle:
         if self.kind == "port":
             self._trig(self.trig)
 
+    def sincos_shift_check(self, chains: int, n_moves: int, step: float, levels: int, seed: int) -> int:
+        """Mismatches of the incremental torsion trig (vs_crtrig sincos_shift)
+        against sincos_cr along random move chains (see vs_oracle.cpp)."""
+        f = self.lib.vso_sincos_shift_check
+        f.restype = C.c_uint64
+        f.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64]
+        return int(f(chains, n_moves, step, levels, seed))
+
     def sincos(self, x: float, correctly_rounded: bool = True):
         s, c = C.c_double(), C.c_double()
         (self._sc_cr if correctly_rounded else self._sc_gl)(x, C.byref(s), C.byref(c))

@@ -1101,6 +1101,48 @@ int vso_detect_torsions(const vs_ligand_batch *b, int i, uint16_t *bonds_out, ui
 
 // The correctly rounded routine the GPU uses (include/vs_crtrig.h), host build.
 void vso_sincos_cr(double x, double *s, double *c) { vs_crtrig::sincos_cr(x, s, c); }
+// The search's incremental torsion trig (vs_crtrig::sincos_shift, what the
+// GPU uses for neighbour angles) along random move chains: starts at lattice
+// angles idx * 2pi/36, applies n_moves moves of +-step * 2^-L (L < levels),
+// compares each result's hi parts with sincos_cr of the new angle.  Returns
+// the number of mismatching sin or cos values out of 2 * chains * n_moves.
+uint64_t vso_sincos_shift_check(int chains, int n_moves, double step, int levels, uint64_t seed) {
+  uint64_t bad = 0, st = seed * 0x9e3779b97f4a7c15ull + 1;
+  auto next = [&st]() {
+    st ^= st << 13;
+    st ^= st >> 7;
+    st ^= st << 17;
+    return st;
+  };
+  const double lattice = 2.0 * 3.14159265358979323846 / 36;
+  for (int ch = 0; ch < chains; ++ch) {
+    double a = static_cast<double>(next() % 36) * lattice;
+    vs_crtrig::dd sa, ca;
+    vs_crtrig::sincos_dd(a, &sa, &ca);
+    for (int k = 0; k < n_moves; ++k) {
+      const int L = static_cast<int>(next() % static_cast<uint64_t>(levels));
+      double d = step;
+      for (int i = 0; i < L; ++i) d *= 0.5;
+      vs_crtrig::dd sd, cd;
+      vs_crtrig::sincos_dd(d, &sd, &cd);
+      if (next() & 1) {
+        d = -d;
+        sd = vs_crtrig::dd_neg(sd);
+      }
+      double an;
+      vs_crtrig::dd sn, cn;
+      if (!vs_crtrig::sincos_shift(a, sa, ca, d, sd, cd, &an, &sn, &cn)) vs_crtrig::sincos_dd(an, &sn, &cn);
+      double es, ec;
+      vs_crtrig::sincos_cr(an, &es, &ec);
+      bad += (sn.hi != es) + (cn.hi != ec);
+      a = an;
+      sa = sn;
+      ca = cn;
+    }
+  }
+  return bad;
+}
+
 void vso_sincos_glibc(double x, double *s, double *c) {
   *s = std::sin(x);
   *c = std::cos(x);

@@ -80,7 +80,7 @@ struct vs_context {
   // flatten / search / select
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
-  DevBuf results, best_ang, best_conf, counters, spin, fibq;
+  DevBuf results, best_ang, best_conf, counters, spin, fibq, stepsc;
   DevBuf aux0, aux1, aux2, aux3, search_args, lig_index;
 };
 
@@ -138,10 +138,17 @@ namespace {
 
 void ensure_lattice(int device) {
   std::call_once(g_lattice_once[device & 63], [] {
-    double sc[72];
+    double sc[72], lo[72];
     constexpr double step = 2.0 * kPi / 36;  // search.cpp:33
-    for (int i = 0; i < 36; ++i) vs_crtrig::sincos_cr(i * step, &sc[2 * i], &sc[2 * i + 1]);
-    vsd::set_lattice_table(sc);
+    for (int i = 0; i < 36; ++i) {
+      vs_crtrig::dd s, c;
+      vs_crtrig::sincos_dd(i * step, &s, &c);
+      sc[2 * i] = s.hi;
+      sc[2 * i + 1] = c.hi;
+      lo[2 * i] = s.lo;
+      lo[2 * i + 1] = c.lo;
+    }
+    vsd::set_lattice_table(sc, lo);
   });
 }
 
@@ -451,13 +458,26 @@ vs_status check_cfg(const vs_scoring_config *cfg) {
 }
 
 vs_status upload_tables(vs_context *ctx, const vs_scoring_config &c, int k, vsd::search_cfg &sc) {
-  std::vector<double> spin, fib;
+  std::vector<double> spin, fib, stepsc;
   const int levels = spin_levels(c);
   spin_table(c, levels, spin);
+  // double-double sin/cos of the torsion step at each level (the search's
+  // incremental neighbour trig, vs_crtrig.h sincos_shift)
+  stepsc.resize(4 * static_cast<size_t>(levels));
+  double dq = c.step_torsion;
+  for (int L = 0; L < levels; ++L, dq *= 0.5) {
+    vs_crtrig::dd s, cc;
+    vs_crtrig::sincos_dd(dq, &s, &cc);
+    stepsc[4 * L] = s.hi;
+    stepsc[4 * L + 1] = s.lo;
+    stepsc[4 * L + 2] = cc.hi;
+    stepsc[4 * L + 3] = cc.lo;
+  }
   fib_table(k, fib);
   vs_status rc;
   if ((rc = h2d(ctx->spin, spin.data(), spin.size(), ctx->stream))) return rc;
   if ((rc = h2d(ctx->fibq, fib.data(), fib.size(), ctx->stream))) return rc;
+  if ((rc = h2d(ctx->stepsc, stepsc.data(), stepsc.size(), ctx->stream))) return rc;
   sc.k = k;
   sc.rescored = c.rescored;
   sc.rmsd_threshold = c.rmsd_threshold;
@@ -470,6 +490,7 @@ vs_status upload_tables(vs_context *ctx, const vs_scoring_config &c, int k, vsd:
   sc.n_levels = levels;
   sc.spin = ctx->spin.as<double>();
   sc.fibq = ctx->fibq.as<double>();
+  sc.stepsc = ctx->stepsc.as<double>();
   // The stream must not outlive the host vectors' copies.
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return VS_OK;

@@ -26,11 +26,10 @@ namespace vsd {
 // CR sin/cos of the 36 flatten lattice angles idx * (2 pi / 36)
 // (search.cpp:33,40), computed on the host with vs_crtrig.
 __constant__ double c_lattice_sc[72];
-constexpr double kPi = 3.14159265358979323846;
 
-void set_lattice_table(const double *sc72) {
+void set_lattice_table(const double *sc72, const double *lo72) {
   cudaMemcpyToSymbol(c_lattice_sc, sc72, sizeof(double) * 72);
-  set_lattice_table_search(sc72);
+  set_lattice_table_search(sc72, lo72);
 }
 
 __device__ __forceinline__ d3 ld3(const double *p) { return {p[0], p[1], p[2]}; }

@@ -74,6 +74,7 @@ struct search_cfg {
   int flatten_sweeps;
   int n_levels;             // spin table levels
   const double *spin;       // [n_levels][6][4] (x,y,z,w), glibc trig, host computed
+  const double *stepsc;     // [n_levels][4] sin hi, sin lo, cos hi, cos lo of step_q * 2^-level
   const double *fibq;       // [k][4]
 };
 
@@ -104,8 +105,8 @@ struct dock_out {
   const int *sweeps;        // flatten sweeps per ligand (flat_out.sweeps)
 };
 
-void set_lattice_table(const double *sc72);
-void set_lattice_table_search(const double *sc72);
+void set_lattice_table(const double *sc72, const double *lo72);
+void set_lattice_table_search(const double *sc72, const double *lo72);
 
 cudaError_t launch_setup(const batch_dev &b, int restarts, cudaStream_t s);
 cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,

@@ -42,10 +42,10 @@ constexpr int kWarps = VS_SEARCH_WARPS;
 #define VS_SEARCH_GROUP 12
 #endif
 constexpr int kGroup = VS_SEARCH_GROUP;  // neighbours per group (>= 12, even; 12 measured best)
-#ifndef VS_RIGID_UNROLL
-#define VS_RIGID_UNROLL 1
+#ifndef VS_SAMPLE_ILP
+#define VS_SAMPLE_ILP 1
 #endif
-constexpr int kRigidUnroll = VS_RIGID_UNROLL;  // rigid samples in flight per lane
+constexpr int kSampleIlp = VS_SAMPLE_ILP;  // samples in flight per lane (1 or 2)
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
@@ -78,9 +78,20 @@ __device__ __forceinline__ d3 rigid_col_a(const double *rt, d3 v, int col) {
   return rigid_col(r, r + 9, v, col);
 }
 
-__device__ __noinline__ void sincos_cr_dev(double a, double *s, double *c) { vs_crtrig::sincos_cr(a, s, c); }
+// sin/cos of a as double-double: hi parts to sc[0], sc[1], lo parts to
+// lo[0], lo[1].  Out of line: the search only needs it at a restart's start
+// (arbitrary angles) and next to zeros of sin/cos (vs_crtrig sincos_shift).
+__device__ __noinline__ void sincos_dd_dev(double a, double *sc, double *lo) {
+  vs_crtrig::dd s, c;
+  vs_crtrig::sincos_dd(a, &s, &c);
+  sc[0] = s.hi;
+  sc[1] = c.hi;
+  lo[0] = s.lo;
+  lo[1] = c.lo;
+}
 
 __constant__ double c_lattice_sc_s[72];
+__constant__ double c_lattice_lo_s[72];  // lo parts of the double-double lattice sin/cos
 
 // Development-only phase profile (build with -DVS_PHASE_PROF): per-warp
 // clock64() time spent in each phase of the search, summed over warps.
@@ -186,6 +197,9 @@ __device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const
   const int t = act ? (v >> 1) : m;
   double *out = Mvar + (act ? mvar_off(v, t, m) : 0);
   int bad = 0;
+#ifdef VS_PHASE_PROF
+  unsigned long long cs_acc = 0;
+#endif
   #pragma unroll 1
   for (int u = vbase >> 1; u < m; ++u) {
     d3 ea = ld3(ep + 6 * u), eb = ld3(ep + 6 * u + 3);
@@ -197,12 +211,23 @@ __device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const
       if ((ma >> w) & 1u) ea = torsion_apply_a(M, ea);
       if ((mb >> w) & 1u) eb = torsion_apply_a(M, eb);
     }
+#ifdef VS_PHASE_PROF
+    __syncwarp();
+    const unsigned long long cs0 = clock64();
+#endif
     if (u >= t) {
       const double s = u == t ? cache[2 * v] : sccur[2 * u];
       const double c = u == t ? cache[2 * v + 1] : sccur[2 * u + 1];
       if (!torsion_setup(ea, eb, s, c, out + 12 * (u - t))) bad = 1;
     }
+#ifdef VS_PHASE_PROF
+    __syncwarp();
+    cs_acc += clock64() - cs0;
+#endif
   }
+#ifdef VS_PHASE_PROF
+  if (lane == 0) atomicAdd(&g_phase[15], cs_acc);
+#endif
   return bad;
 }
 
@@ -245,8 +270,10 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   double *vcur = W + A.o_vcur;
   double *scores = W + A.o_scores;
   double *cache = W + A.o_cache;
+  double *cachelo = cache + 4 * A.mmax;
   double *ang = W + A.o_ang;
   double *sccur = W + A.o_sccur;
+  double *sclo = sccur + 2 * A.mmax;
   double *S = W + A.o_state;
   int *cvalid = reinterpret_cast<int *>(W + A.o_ints);
 
@@ -315,7 +342,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     if (A.ang_in) {  // local_search / initial_poses entry points: arbitrary angles
       for (int u = lane; u < m; u += 32) {
         ang[u] = A.ang_in[t0 + u];
-        sincos_cr_dev(ang[u], &sccur[2 * u], &sccur[2 * u + 1]);
+        sincos_dd_dev(ang[u], &sccur[2 * u], &sclo[2 * u]);
       }
     } else {
       for (int u = lane; u < m; u += 32) {
@@ -323,6 +350,8 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         ang[u] = li * kLatticeStep;  // angles_of, search.cpp:40
         sccur[2 * u] = c_lattice_sc_dev(2 * li);
         sccur[2 * u + 1] = c_lattice_sc_dev(2 * li + 1);
+        sclo[2 * u] = c_lattice_lo_s[2 * li];
+        sclo[2 * u + 1] = c_lattice_lo_s[2 * li + 1];
       }
     }
     if (lane == 0) S[S_ERR] = 0.0;
@@ -461,8 +490,24 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         for (int vb0 = 0; vb0 < 2 * m; vb0 += 32) {
           const int v = vb0 + lane;
           if (v < 2 * m && !cvalid[v]) {
-            const double sign = (v & 1) ? -1.0 : 1.0;
-            sincos_cr_dev(ang[v >> 1] + sign * step_q, &cache[2 * v], &cache[2 * v + 1]);
+            // sin/cos of ang[t] +- step_q from the current double-double
+            // values and the level's step table (vs_crtrig.h sincos_shift)
+            const int t = v >> 1;
+            const double *st = A.c.stepsc + 4 * level;
+            const bool neg = v & 1;
+            const vs_crtrig::dd sd{neg ? -st[0] : st[0], neg ? -st[1] : st[1]}, cd{st[2], st[3]};
+            double an;
+            vs_crtrig::dd sn, cn;
+            if (!vs_crtrig::sincos_shift(ang[t], vs_crtrig::dd{sccur[2 * t], sclo[2 * t]},
+                                         vs_crtrig::dd{sccur[2 * t + 1], sclo[2 * t + 1]}, neg ? -step_q : step_q, sd,
+                                         cd, &an, &sn, &cn)) {
+              sincos_dd_dev(an, &cache[2 * v], &cachelo[2 * v]);
+            } else {
+              cache[2 * v] = sn.hi;
+              cache[2 * v + 1] = cn.hi;
+              cachelo[2 * v] = sn.lo;
+              cachelo[2 * v + 1] = cn.lo;
+            }
             cvalid[v] = 1;
           }
           __syncwarp();
@@ -514,41 +559,78 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           jn = 2 * (thi - tlo);
           items = 2 * (s_doff[thi - 1] + s_dcnt[thi - 1] - s_doff[tlo]);
         }
-        // Two items per lane per step (independent gathers in flight); the
-        // rigid and the torsion neighbours run in separate compact loops.
-        // Rigid and torsion neighbours run in separate compact loops, one
-        // sample per lane per step: the search is instruction-fetch bound
-        // when warps at different phases share an SM, so the hot code is
-        // kept small (measured: 1 sample in flight beats 2 or 3).
+        // Rigid and torsion neighbours run in separate compact loops (the hot
+        // code must stay small: the search was instruction-fetch bound).
+        // With kSampleIlp == 2 each lane computes two samples before storing
+        // either, so their load/FP64 latency chains overlap (a store between
+        // them would order the second sample's shared loads after it).
         if (grp == 0) {
           // rigid neighbours: lane = heavy atom, loop over the 12 transforms
           // (their matrices are warp-uniform shared-memory broadcasts)
           for (int h = lane; h < n; h += 32) {
             const int a = s_hl[h];
             const d3 x = ld3(tors + 3 * a);
-            #pragma unroll kRigidUnroll
-            for (int j = 0; j < 12; ++j) {
-              const double *X = Rj + 16 * j;
-              bool out;
-              vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(X, x, a), out);
+            if (kSampleIlp == 2) {
+              #pragma unroll 1
+              for (int j = 0; j < 12; j += 2) {
+                bool o0, o1;
+                const double v0 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(Rj + 16 * j, x, a), o0);
+                const double v1 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(Rj + 16 * (j + 1), x, a), o1);
+                vb[j * nmax + h] = v0;
+                vb[(j + 1) * nmax + h] = v1;
+              }
+            } else {
+              #pragma unroll 1
+              for (int j = 0; j < 12; ++j) {
+                bool out;
+                vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(Rj + 16 * j, x, a), out);
+              }
             }
           }
         } else {
           const uint32_t *ti = s_tit + 2 * s_doff[tlo];
-          for (int it = lane; it < items; it += 32) {
-            const uint32_t e = ti[it];
-            const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
-            d3 x = ld3(s_bh + 3 * h);
-            const uint32_t mask = s_tmh[h];
-            const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
-            #pragma unroll 1
-            for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
-              const int u = __ffs(bb) - 1;
-              x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
+          if (kSampleIlp == 2) {
+            for (int it = lane; it < items; it += 64) {
+              const bool two = it + 32 < items;
+              const uint32_t e0 = ti[it], e1 = two ? ti[it + 32] : e0;
+              const int v0 = (e0 >> 8) & 63, h0 = e0 & 255, t0 = v0 >> 1;
+              const int v1 = (e1 >> 8) & 63, h1 = e1 & 255, t1 = v1 >> 1;
+              d3 x0 = ld3(s_bh + 3 * h0), x1 = ld3(s_bh + 3 * h1);
+              const uint32_t k0 = s_tmh[h0], k1 = s_tmh[h1];
+              const double *M0 = Mvar + mvar_off(v0, t0, m) - 12 * t0;
+              const double *M1 = Mvar + mvar_off(v1, t1, m) - 12 * t1;
+              #pragma unroll 1
+              for (uint32_t bb = k0 & 0x7fffffffu; bb; bb &= bb - 1u) {
+                const int u = __ffs(bb) - 1;
+                x0 = torsion_apply_a((u < t0 ? Mcur : M0) + 12 * u, x0);
+              }
+              #pragma unroll 1
+              for (uint32_t bb = two ? (k1 & 0x7fffffffu) : 0u; bb; bb &= bb - 1u) {
+                const int u = __ffs(bb) - 1;
+                x1 = torsion_apply_a((u < t1 ? Mcur : M1) + 12 * u, x1);
+              }
+              bool o0, o1;
+              const double f0 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x0, (int)(k0 >> 31)), o0);
+              const double f1 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x1, (int)(k1 >> 31)), o1);
+              vb[(v0 - 2 * tlo) * nmax + h0] = f0;
+              if (two) vb[(v1 - 2 * tlo) * nmax + h1] = f1;
             }
-            bool out;
-            vb[(v - 2 * tlo) * nmax + h] =
-                field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x, (int)(mask >> 31)), out);
+          } else {
+            for (int it = lane; it < items; it += 32) {
+              const uint32_t e = ti[it];
+              const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
+              d3 x = ld3(s_bh + 3 * h);
+              const uint32_t mask = s_tmh[h];
+              const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
+              #pragma unroll 1
+              for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
+                const int u = __ffs(bb) - 1;
+                x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
+              }
+              bool out;
+              vb[(v - 2 * tlo) * nmax + h] =
+                  field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x, (int)(mask >> 31)), out);
+            }
           }
         }
         __syncwarp();
@@ -612,6 +694,8 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             ang[t] = ang[t] + sign * step_q;
             sccur[2 * t] = cache[2 * v];
             sccur[2 * t + 1] = cache[2 * v + 1];
+            sclo[2 * t] = cachelo[2 * v];
+            sclo[2 * t + 1] = cachelo[2 * v + 1];
           }
           if (lane < 2) cvalid[2 * t + lane] = 0;
           mvar_valid = false;
@@ -703,9 +787,9 @@ Layout layout(int Nm, int nm, int mm, int dm) {
   L.o_vbest = take(nm);
   L.o_vcur = take(nm);
   L.o_scores = take(kGroup);
-  L.o_cache = take(4 * mm);
+  L.o_cache = take(8 * mm);  // sin/cos of the 2m variant angles: hi parts, then lo parts
   L.o_ang = take(mm);
-  L.o_sccur = take(2 * mm);
+  L.o_sccur = take(4 * mm);  // sin/cos of the current angles: hi parts, then lo parts
   L.o_state = take(S_N);
   L.o_ints = take((2 * mm + 1) / 2 + 1);
   L.total = o;
@@ -739,6 +823,9 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
+#ifdef VS_PROF_CTAS_PER_SM
+  per_sm = VS_PROF_CTAS_PER_SM;  // development: phase timing without co-resident warps
+#endif
   int blocks = num_sms * per_sm;
   if (blocks > A.n_lig) blocks = A.n_lig;
   if (blocks < 1) blocks = 1;
@@ -754,7 +841,10 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
 
 }  // namespace
 
-void set_lattice_table_search(const double *sc72) { cudaMemcpyToSymbol(c_lattice_sc_s, sc72, sizeof(double) * 72); }
+void set_lattice_table_search(const double *sc72, const double *lo72) {
+  cudaMemcpyToSymbol(c_lattice_sc_s, sc72, sizeof(double) * 72);
+  cudaMemcpyToSymbol(c_lattice_lo_s, lo72, sizeof(double) * 72);
+}
 
 #ifdef VS_PHASE_PROF
 extern "C" int vs_debug_phase_read(unsigned long long *out, int reset) {

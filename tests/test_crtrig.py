@@ -50,3 +50,14 @@ def test_glibc_disagreement_is_rare(port):
     xs = rng.uniform(-10, 10, 20000)
     diff = sum(port.sincos(float(x), True) != port.sincos(float(x), False) for x in xs)
     assert diff / xs.size < 0.01
+
+
+def test_incremental_shift_matches_correct_rounding(port):
+    """The search derives neighbour sin/cos incrementally (angle addition in
+    double-double, vs_crtrig.h sincos_shift); along 20k random chains of 60
+    moves (2.4M values, default and tiny steps) every hi part equals the
+    correctly rounded sin/cos of the new angle."""
+    step = 20.0 * math.pi / 180.0
+    assert port.sincos_shift_check(20000, 60, step, 4, 1) == 0
+    assert port.sincos_shift_check(2000, 60, step, 40, 2) == 0
+    assert port.sincos_shift_check(2000, 200, 1.0, 8, 3) == 0

@@ -38,7 +38,8 @@ def main():
     print(f"iterations {buf[11]}, with matrix rebuild {buf[10]} ({100.0 * buf[10] / max(buf[11], 1):.1f} %)")
     nb = max(buf[10], 1)
     print(f"per rebuild (max over lanes): sincos {buf[12] / nb:.0f}  chain {buf[13] / nb:.0f}  "
-          f"rigid transforms {buf[14] / nb:.0f} cycles; whole rebuild phase {buf[9] / nb:.0f}")
+          f"rigid transforms {buf[14] / nb:.0f} cycles; whole rebuild phase {buf[9] / nb:.0f}; "
+          f"of the chain: matrix setups {buf[15] / nb:.0f}")
     for i, name in enumerate(NAMES):
         print(f"{name:32s} {100.0 * buf[i] / tot:6.2f} %   {buf[i] / 1e9:10.3f} Gcycles")
 
