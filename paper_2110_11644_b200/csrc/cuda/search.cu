@@ -183,6 +183,8 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
 }
 
 // Torsion-neighbour matrices of variants vbase + lane (search.cpp:168-176:
+// (matrices of torsions u < ufrom are still valid: after a move of torsion
+// ufrom only the matrices from ufrom on change)
 // torsion t = v / 2 moved by +-step), warp-cooperative: all lanes walk the
 // torsions u in the same order, so the endpoint masks (ep/epm: base
 // coordinates and torsion masks of torsion u's bond atoms) and the branches
@@ -190,8 +192,9 @@ __device__ __noinline__ bool chain_mats(int t, double st, double ct, int m, cons
 // (w < t) and through its own new matrices (t <= w < u), then builds matrix
 // u once u >= t -- chain_mats' arithmetic, lanes in lockstep instead of
 // diverging on different chain lengths.  Returns nonzero on a degenerate axis.
-__device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const uint32_t *epm, const double *Mcur,
-                                       const double *sccur, const double *cache, double *Mvar, int lane) {
+__device__ __noinline__ int chain_warp(int vbase, int ufrom, int m, const double *ep, const uint32_t *epm,
+                                       const double *Mcur, const double *sccur, const double *cache, double *Mvar,
+                                       int lane) {
   const int v = vbase + lane;
   const bool act = v < 2 * m;
   const int t = act ? (v >> 1) : m;
@@ -201,15 +204,20 @@ __device__ __noinline__ int chain_warp(int vbase, int m, const double *ep, const
   unsigned long long cs_acc = 0;
 #endif
   #pragma unroll 1
-  for (int u = vbase >> 1; u < m; ++u) {
+  for (int u = max(vbase >> 1, ufrom); u < m; ++u) {
     d3 ea = ld3(ep + 6 * u), eb = ld3(ep + 6 * u + 3);
     const uint32_t ma = epm[2 * u], mb = epm[2 * u + 1];
     #pragma unroll 1
     for (uint32_t bb = (ma | mb) & ((1u << u) - 1u); bb; bb &= bb - 1u) {
       const int w = __ffs(bb) - 1;
       const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
-      if ((ma >> w) & 1u) ea = torsion_apply_a(M, ea);
-      if ((mb >> w) & 1u) eb = torsion_apply_a(M, eb);
+      // both endpoints in one block (shared matrix loads, overlapping
+      // chains), then keep the ones torsion w moves
+      double r[12];
+      ld12a(M, r);
+      const d3 na = torsion_apply(r, ea), nb = torsion_apply(r, eb);
+      if ((ma >> w) & 1u) ea = na;
+      if ((mb >> w) & 1u) eb = nb;
     }
 #ifdef VS_PHASE_PROF
     __syncwarp();
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     // ---- local_search (search.cpp:121-191)
     int level = 0, n_iter = 0, n_adopt = 0;
     bool failed = false, mvar_valid = false, moved = false;
+    int chain_from = 0;  // first torsion whose neighbour matrices are stale
     for (int iter = 0; iter < A.c.max_iter && S[S_STEPT] >= A.c.min_t; ++iter) {
       const double step_t = S[S_STEPT], step_q = S[S_STEPQ];
       // rigid neighbour transforms (lanes 0-11) and, when stale, the
@@ -515,7 +524,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           pr_sc += (unsigned int)(clock64() - pr0);
           pr0 = clock64();
 #endif
-          if (chain_warp(vb0, m, s_ep, s_epm, Mcur, sccur, cache, Mvar, lane)) S[S_ERR] = 1.0;
+          if (chain_warp(vb0, chain_from, m, s_ep, s_epm, Mcur, sccur, cache, Mvar, lane)) S[S_ERR] = 1.0;
 #ifdef VS_PHASE_PROF
           __syncwarp();
           pr_ch += (unsigned int)(clock64() - pr0);
@@ -699,6 +708,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           }
           if (lane < 2) cvalid[2 * t + lane] = 0;
           mvar_valid = false;
+          chain_from = t;
           __syncwarp();
           #pragma unroll 1
           for (int a = lane; a < N; a += 32) {
@@ -724,6 +734,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         }
         for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
         mvar_valid = false;
+        chain_from = 0;
         ++level;
         PH(7)
       }
