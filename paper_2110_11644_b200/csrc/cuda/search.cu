@@ -243,6 +243,7 @@ __device__ __noinline__ int chain_warp(int vbase, int ufrom, int m, const double
 // the transformed coordinates to `scratch`, then three lanes run the
 // Eigen-order row sums (dmath.cuh centroid_row).  One out-of-line copy.
 __device__ __noinline__ void compute_pivot(double *scratch, const double *tors, double *S, int N, int lane) {
+  #pragma unroll 1
   for (int a = lane; a < N; a += 32) st3(scratch + 3 * a, rigid_col_a(S + S_R, ld3(tors + 3 * a), a));
   __syncwarp();
   if (lane < 3) S[S_PIV + lane] = centroid_row(scratch, N, lane);
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     const int l = A.lig_index ? A.lig_index[li] : li;
     const lig_meta meta = b.meta[l];
     if (meta.status != VS_LIG_OK) {
+      #pragma unroll 1
       for (int r = threadIdx.x; r < k; r += blockDim.x) A.o.status[l * k + r] = meta.status;
       continue;
     }
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       const uint16_t *hl = b.heavy_list + a0;
       const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
       const uint32_t *titems = b.titems + 2 * b.ditem_base[l];
+      #pragma unroll 1
       for (int h = threadIdx.x; h < n; h += blockDim.x) {
         const int a = hl[h];
         st3(s_bh + 3 * h, ld3(base + 3 * a));
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         s_dm[h] = b.heavy_dmask[a0 + h];
         s_hl[h] = (uint32_t)a;
       }
+      #pragma unroll 1
       for (int u = threadIdx.x; u < m; u += blockDim.x) {
         const int ea = ta[u], eb = tb[u];
         st3(s_ep + 6 * u, ld3(base + 3 * ea));
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         s_doff[u] = b.d_off[t0 + u];
         s_dcnt[u] = b.d_count[t0 + u];
       }
+      #pragma unroll 1
       for (int i = threadIdx.x; i < 2 * meta.d_total; i += blockDim.x) s_tit[i] = titems[i];
     }
     __syncthreads();
@@ -346,13 +351,16 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     unsigned long long evals = 0;
 
     // ---- per-restart tables
+    #pragma unroll 1
     for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
     if (A.ang_in) {  // local_search / initial_poses entry points: arbitrary angles
+      #pragma unroll 1
       for (int u = lane; u < m; u += 32) {
         ang[u] = A.ang_in[t0 + u];
         sincos_dd_dev(ang[u], &sccur[2 * u], &sclo[2 * u]);
       }
     } else {
+      #pragma unroll 1
       for (int u = lane; u < m; u += 32) {
         const int li = A.f.idx[t0 + u];
         ang[u] = li * kLatticeStep;  // angles_of, search.cpp:40
@@ -418,6 +426,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       S[S_STEPQ] = A.c.step_q;
     }
     __syncwarp();
+    #pragma unroll 1
     for (int h = lane; h < n; h += 32) {
       const int a = s_hl[h];
       bool out;
@@ -576,6 +585,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         if (grp == 0) {
           // rigid neighbours: lane = heavy atom, loop over the 12 transforms
           // (their matrices are warp-uniform shared-memory broadcasts)
+          #pragma unroll 1
           for (int h = lane; h < n; h += 32) {
             const int a = s_hl[h];
             const d3 x = ld3(tors + 3 * a);
@@ -625,6 +635,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
               if (two) vb[(v1 - 2 * tlo) * nmax + h1] = f1;
             }
           } else {
+            #pragma unroll 1
             for (int it = lane; it < items; it += 32) {
               const uint32_t e = ti[it];
               const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
@@ -675,9 +686,11 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           bj = j0 + gj;
           const double *row = vb + gj * nmax;
           if (grp == 0) {
+            #pragma unroll 1
             for (int h = lane; h < n; h += 32) vbest[h] = row[h];
           } else {
             const int t = tlo + (gj >> 1);
+            #pragma unroll 1
             for (int h = lane; h < n; h += 32) vbest[h] = ((s_dm[h] >> t) & 1u) ? row[h] : vcur[h];
           }
         }
@@ -732,6 +745,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           S[S_STEPR] = S[S_STEPR] * 0.5;
           S[S_STEPQ] = S[S_STEPQ] * 0.5;
         }
+        #pragma unroll 1
         for (int v = lane; v < 2 * m; v += 32) cvalid[v] = 0;
         mvar_valid = false;
         chain_from = 0;
@@ -748,12 +762,15 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     // local_search mode an unmoved pose returns its input conformation.
     const size_t ck = 3 * ((size_t)a0 * k + (size_t)r * N);
     if (ls_mode && !moved) {
+      #pragma unroll 1
       for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
     } else {
+      #pragma unroll 1
       for (int a = lane; a < N; a += 32)
         st3(A.o.conf + ck + 3 * a, rigid_col_a(S + S_R, ld3(tors + 3 * a), a));
     }
     const size_t tk = (size_t)t0 * k + (size_t)r * m;
+    #pragma unroll 1
     for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = ang[u];
     if (lane < 4)
       A.o.T[7 * (size_t)item + lane] = S[S_Q + lane];
