@@ -234,14 +234,14 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
 #pragma unroll
               for (int q = 0; q < kFlatUnroll; ++q) {
                 const d3 xj{C[(3 * (j + q)) * CB], C[(3 * (j + q) + 1) * CB], C[(3 * (j + q) + 2) * CB]};
-                d[q] = dsqrt(sqn3(sub3(xi, xj)));
+                d[q] = dsqrt_dist2(sqn3(sub3(xi, xj)));
               }
 #pragma unroll
               for (int q = 0; q < kFlatUnroll; ++q) sum += d[q];
             }
             for (; j < N; ++j) {
               const d3 xj{C[(3 * j) * CB], C[(3 * j + 1) * CB], C[(3 * j + 2) * CB]};
-              sum += dsqrt(sqn3(sub3(xi, xj)));
+              sum += dsqrt_dist2(sqn3(sub3(xi, xj)));
             }
           }
           spread[o] = sum;

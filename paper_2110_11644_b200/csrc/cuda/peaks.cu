@@ -102,7 +102,9 @@ __global__ void k_sqrt_check(uint64_t n, uint64_t seed, unsigned long long *bad,
     }
     if (!(x >= 0.0)) continue;
     const double a = vsd::dsqrt(x), b = sqrt(x);
-    if (__double_as_longlong(a) != __double_as_longlong(b)) {
+    // dsqrt_dist2 (k_flatten's pair distances) on its domain: 0 or >= 2^-1000
+    const double a2 = (x == 0.0 || x >= 0x1p-1000) ? vsd::dsqrt_dist2(x) : b;
+    if (__double_as_longlong(a) != __double_as_longlong(b) || __double_as_longlong(a2) != __double_as_longlong(b)) {
       if (atomicAdd(bad, 1ull) == 0) *first = (unsigned long long)__double_as_longlong(x);
     }
   }
