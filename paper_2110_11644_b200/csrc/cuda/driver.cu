@@ -80,7 +80,7 @@ struct vs_context {
   // flatten / search / select
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
-  DevBuf results, best_ang, best_conf, counters, spin, fibq, stepsc;
+  DevBuf results, best_ang, best_conf, counters, spin, fibq, stepsc, flat_index;
   DevBuf aux0, aux1, aux2, aux3, search_args, lig_index;
 };
 
@@ -457,6 +457,38 @@ vs_status check_cfg(const vs_scoring_config *cfg) {
   return VS_OK;
 }
 
+// k_flatten's shared memory is 37 copies of a ligand's coordinates, sized by
+// the largest ligand of the launch: ligands are launched in atom-count
+// buckets so small ligands get more resident CTAs per SM.
+vs_status flatten_buckets(vs_context *ctx, const Staged &st, int max_sweeps, const vsd::flat_out &f) {
+  static const int kLimits[] = {40, 48, 56, 64, 72, 80, 96, 128, 1 << 30};
+  constexpr int kB = sizeof(kLimits) / sizeof(kLimits[0]);
+  std::vector<int> order;
+  order.reserve(static_cast<size_t>(st.n));
+  int start[kB + 1] = {0}, nmax[kB] = {0};
+  for (int bi = 0; bi < kB; ++bi) {
+    start[bi] = static_cast<int>(order.size());
+    const int lo = bi ? kLimits[bi - 1] : 0;
+    for (int i = 0; i < st.n; ++i)
+      if (st.lN[i] > lo && st.lN[i] <= kLimits[bi]) {
+        order.push_back(i);
+        nmax[bi] = std::max(nmax[bi], st.lN[i]);
+      }
+  }
+  start[kB] = static_cast<int>(order.size());  // (N == 0 ligands: rejected by k_setup, no flatten)
+  vs_status rc;
+  if ((rc = h2d(ctx->flat_index, order.data(), order.size(), ctx->stream))) return rc;
+  for (int bi = 0; bi < kB; ++bi) {
+    const int cnt = start[bi + 1] - start[bi];
+    if (cnt == 0) continue;
+    CUDA_TRY(vsd::launch_flatten(st.b, max_sweeps, f, std::max(nmax[bi], 1), st.mmax, ctx->stream,
+                                 ctx->flat_index.as<int>() + start[bi], cnt));
+    ++ctx->last_launches;
+  }
+  --ctx->last_launches;  // one flatten launch is counted with the fixed stages
+  return VS_OK;
+}
+
 vs_status upload_tables(vs_context *ctx, const vs_scoring_config &c, int k, vsd::search_cfg &sc) {
   std::vector<double> spin, fib, stepsc;
   const int levels = spin_levels(c);
@@ -780,7 +812,7 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     std::vector<vsd::lig_meta> meta(static_cast<size_t>(std::max(st.n, 1)));
     CUDA_TRY(cudaMemcpyAsync(meta.data(), st.b.meta, sizeof(vsd::lig_meta) * st.n, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
-    CUDA_TRY(vsd::launch_flatten(st.b, cfg->flatten_max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
+    if ((rc = flatten_buckets(ctx, st, cfg->flatten_max_sweeps, f))) return rc;
     CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
     CUDA_TRY(ctx->search_args.ensure(vsd::search_args_bytes()));
     CUDA_TRY(cudaEventSynchronize(ctx->ev1));
@@ -916,7 +948,7 @@ vs_status vs_flatten_batch(vs_context *ctx, const vs_ligand_batch *batch, int32_
   vsd::flat_out f{};
   if ((rc = ensure_flat(ctx, st, f))) return rc;
   CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
-  CUDA_TRY(vsd::launch_flatten(st.b, max_sweeps, f, std::max(st.Nmax, 1), st.mmax, ctx->stream));
+  if ((rc = flatten_buckets(ctx, st, max_sweeps, f))) return rc;
   std::vector<int> idx(static_cast<size_t>(std::max(st.torsions, 1)));
   std::vector<vsd::lig_meta> meta(static_cast<size_t>(std::max(st.n, 1)));
   if (st.atoms)

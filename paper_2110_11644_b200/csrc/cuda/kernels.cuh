@@ -110,7 +110,7 @@ void set_lattice_table_search(const double *sc72, const double *lo72);
 
 cudaError_t launch_setup(const batch_dev &b, int restarts, cudaStream_t s);
 cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,
-                           cudaStream_t s);
+                           cudaStream_t s, const int *lig_index = nullptr, int n_lig = 0);
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf,
