@@ -165,9 +165,10 @@ __device__ __forceinline__ void lattice_sc(int idx, double &s, double &c) {
   c = c_lattice_sc[2 * idx + 1];
 }
 
-__global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_sweeps, flat_out f, int cand_per_round) {
+__global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_sweeps, flat_out f, int cand_per_round,
+                                                          const int *lig_index) {
   extern __shared__ double sm[];
-  const int l = blockIdx.x;
+  const int l = lig_index ? lig_index[blockIdx.x] : blockIdx.x;
   const int tid = threadIdx.x;
   const lig_meta meta = b.meta[l];
   const int a0 = b.atom_off[l], t0 = b.tors_off[l];
@@ -307,15 +308,16 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
 }
 
 cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,
-                           cudaStream_t s) {
-  if (b.n_lig == 0) return cudaSuccess;
+                           cudaStream_t s, const int *lig_index, int n_lig) {
+  const int n = lig_index ? n_lig : b.n_lig;
+  if (n == 0) return cudaSuccess;
   (void)mmax;
   int cb = 36;
   auto bytes = [&](int c) { return (size_t)(3 * nmax_atoms * (1 + c) + 36 + 12) * sizeof(double); };
   while (cb > 1 && bytes(cb) > 200 * 1024) cb = (cb + 1) / 2;
   const size_t smem = bytes(cb);
   cudaFuncSetAttribute(k_flatten, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_flatten<<<b.n_lig, kFlatThreads, smem, s>>>(b, max_sweeps, f, cb);
+  k_flatten<<<n, kFlatThreads, smem, s>>>(b, max_sweeps, f, cb, lig_index);
   return cudaGetLastError();
 }
 
