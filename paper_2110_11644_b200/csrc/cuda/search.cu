@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../../include/vs_crtrig.h"
 #include "../../../include/vs_dock.h"
@@ -857,6 +859,9 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   int blocks = num_sms * per_sm;
   if (blocks > A.n_lig) blocks = A.n_lig;
   if (blocks < 1) blocks = 1;
+  if (std::getenv("VSDOCK_DEBUG"))
+    std::fprintf(stderr, "k_search: %d ligands, N<=%d n<=%d m<=%d d<=%d, smem %zu B/CTA, %d CTAs/SM, %d CTAs\n", A.n_lig,
+                 A.Nmax, A.nmax, A.mmax, A.dmax, smem, per_sm, blocks);
   if (A.pg.mode == 1)
     k_search<1><<<blocks, 32 * kWarps, smem, s>>>(A);
   else if (A.pg.mode == 2)
