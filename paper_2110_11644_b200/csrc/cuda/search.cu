@@ -43,11 +43,8 @@ constexpr int kWarps = VS_SEARCH_WARPS;
 #ifndef VS_SEARCH_GROUP
 #define VS_SEARCH_GROUP 12
 #endif
+constexpr int kRow = 18;  // spin-neighbour row: R (9), pad, t (3), pad, q (4)
 constexpr int kGroup = VS_SEARCH_GROUP;  // neighbours per group (>= 12, even; 12 measured best)
-#ifndef VS_SAMPLE_ILP
-#define VS_SAMPLE_ILP 1
-#endif
-constexpr int kSampleIlp = VS_SAMPLE_ILP;  // samples in flight per lane (1 or 2)
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kLatticeStep = 2.0 * kPi / 36;
 
@@ -78,6 +75,23 @@ __device__ __forceinline__ d3 rigid_col_a(const double *rt, d3 v, int col) {
   double r[12];
   ld12a(rt, r);
   return rigid_col(r, r + 9, v, col);
+}
+// Rotation (9 doubles) and translation (3) at two 16-byte aligned addresses.
+__device__ __forceinline__ d3 rigid_col_rt(const double *R, const double *T, d3 v, int col) {
+  double r[9], t[3];
+  const double2 *q = reinterpret_cast<const double2 *>(R);
+  #pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double2 w = q[i];
+    r[2 * i] = w.x;
+    r[2 * i + 1] = w.y;
+  }
+  r[8] = R[8];
+  const double2 w = *reinterpret_cast<const double2 *>(T);
+  t[0] = w.x;
+  t[1] = w.y;
+  t[2] = T[2];
+  return rigid_col(r, t, v, col);
 }
 
 // sin/cos of a as double-double: hi parts to sc[0], sc[1], lo parts to
@@ -147,10 +161,11 @@ struct search_args {
   int *work;
   int n_lig;             // ligands of this launch (each: k restarts)
   const int *lig_index;  // bucket launches: launch ligand -> batch ligand (NULL: identity)
+  double *hscr;          // per resident warp: 3 * Nmax doubles (hydrogens' torsioned frame)
   int Nmax, nmax, mmax, dmax;
   int warp_doubles;
   int cta_doubles;       // CTA-shared ligand staging (after the palette)
-  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints;
+  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_cache, o_ang, o_sccur, o_state, o_ints;
 };
 
 // Offset (in doubles) of variant v's matrix for torsion u >= t(v) inside the
@@ -241,12 +256,49 @@ __device__ __noinline__ int chain_warp(int vbase, int ufrom, int m, const double
   return bad;
 }
 
-// Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
-// the transformed coordinates to `scratch`, then three lanes run the
-// Eigen-order row sums (dmath.cuh centroid_row).  One out-of-line copy.
-__device__ __noinline__ void compute_pivot(double *scratch, const double *tors, double *S, int N, int lane) {
+// Torsioned frame (search.cpp:115) of the hydrogens into the warp's global
+// scratch `hx` (atom order; apply_torsions per atom, transform.cpp:73-81).
+// The search keeps only heavy atoms in shared memory: hydrogens matter only
+// for pivots and outputs.
+__device__ __noinline__ void hydrogen_frame(double *hx, int N, const double *base, const uint32_t *tm,
+                                            const uint8_t *heavy, const double *Mcur, int lane) {
   #pragma unroll 1
-  for (int a = lane; a < N; a += 32) st3(scratch + 3 * a, rigid_col_a(S + S_R, ld3(tors + 3 * a), a));
+  for (int a = lane; a < N; a += 32) {
+    if (heavy[a]) continue;
+    d3 x = ld3(base + 3 * a);
+    #pragma unroll 1
+    for (uint32_t bb = tm[a]; bb; bb &= bb - 1u) x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
+    st3(hx + 3 * a, x);
+  }
+}
+
+// The whole conformation of the current pose into `out` (3N, atom order):
+// heavy atoms from the shared-memory frame `torsh`, hydrogens from `hx`,
+// then apply_rigid (transform.cpp:31) when `rigid`.
+__device__ __noinline__ void full_conformation(double *out, const double *torsh, const double *S, const uint32_t *hl,
+                                               int n, int N, const double *hx, const uint8_t *heavy, bool rigid,
+                                               int lane) {
+  #pragma unroll 1
+  for (int h = lane; h < n; h += 32) {
+    const int a = hl[h];
+    const d3 x = ld3(torsh + 3 * h);
+    st3(out + 3 * a, rigid ? rigid_col_a(S + S_R, x, a) : x);
+  }
+  #pragma unroll 1
+  for (int a = lane; a < N; a += 32) {
+    if (heavy[a]) continue;
+    const d3 x = ld3(hx + 3 * a);
+    st3(out + 3 * a, rigid ? rigid_col_a(S + S_R, x, a) : x);
+  }
+}
+
+// Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
+// the transformed conformation to `scratch`, then three lanes run the
+// Eigen-order row sums (dmath.cuh centroid_row).
+__device__ __forceinline__ void compute_pivot(double *scratch, const double *torsh, double *S, const uint32_t *hl,
+                                              int n, int N, const double *hx, const uint8_t *heavy, bool rigid,
+                                              int lane) {
+  full_conformation(scratch, torsh, S, hl, n, N, hx, heavy, rigid, lane);
   __syncwarp();
   if (lane < 3) S[S_PIV + lane] = centroid_row(scratch, N, lane);
   __syncwarp();
@@ -269,17 +321,18 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   uint32_t *s_epm = s_hl + A.nmax;        // 2 * mmax: torsion masks of the endpoints
   int *s_doff = reinterpret_cast<int *>(s_epm + 2 * A.mmax);  // mmax
   int *s_dcnt = s_doff + A.mmax;          // mmax
-  uint32_t *s_tit = reinterpret_cast<uint32_t *>(s_dcnt + A.mmax);  // 2 * dmax torsion-neighbour items
+  uint32_t *s_tit = reinterpret_cast<uint32_t *>(s_dcnt + A.mmax);  // dmax: (t, h in D_t) pairs, h | 2t << 8
   __shared__ int sh_lig, sh_r;
   double *W = sm + 16 + A.cta_doubles + (size_t)warp * A.warp_doubles;
-  double *tors = W + A.o_tors;
+  double *torsh = W + A.o_tors;  // 3 * nmax: torsioned frame of the heavy atoms (search.cpp:115)
+  double *hx = A.hscr + (size_t)(blockIdx.x * kWarps + warp) * 3 * A.Nmax;  // hydrogens' frame (global)
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
-  double *Rj = W + A.o_Rj;
+  double *Rj = W + A.o_Rj;       // 6 spin neighbours x kRow: R at 0, t at 10, q at 14 (16-byte aligned)
+  double *Tj = Rj + 6 * kRow;    // 6 translation neighbours' t, stride 4
   double *vb = W + A.o_vb;
   double *vbest = W + A.o_vbest;
   double *vcur = W + A.o_vcur;
-  double *scores = W + A.o_scores;
   double *cache = W + A.o_cache;
   double *cachelo = cache + 4 * A.mmax;
   double *ang = W + A.o_ang;
@@ -316,6 +369,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     const int a0 = b.atom_off[l], t0 = b.tors_off[l];
     const double *base = b.xyz + 3 * (size_t)a0;
     const uint32_t *tm = b.atom_tmask + a0;
+    const uint8_t *hv = b.heavy + a0;
     {
       const uint16_t *hl = b.heavy_list + a0;
       const uint16_t *ta = b.tors_a + t0, *tb = b.tors_b + t0;
@@ -338,8 +392,13 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         s_doff[u] = b.d_off[t0 + u];
         s_dcnt[u] = b.d_count[t0 + u];
       }
+      // the (t,+) half of k_setup's item list: (t,-) items pair with them
       #pragma unroll 1
-      for (int i = threadIdx.x; i < 2 * meta.d_total; i += blockDim.x) s_tit[i] = titems[i];
+      for (int u = threadIdx.x; u < m; u += blockDim.x) {
+        const int off = b.d_off[t0 + u], cnt = b.d_count[t0 + u];
+        #pragma unroll 1
+        for (int i = 0; i < cnt; ++i) s_tit[off + i] = titems[2 * off + i];
+      }
     }
     __syncthreads();
     const int J = 12 + 2 * m;
@@ -381,21 +440,22 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
       continue;
     }
-    // torsioned frame (search.cpp:115)
+    // torsioned frame (search.cpp:115), heavy atoms
     #pragma unroll 1
-    for (int a = lane; a < N; a += 32) {
-      d3 x = ld3(base + 3 * a);
-      const uint32_t mask = tm[a];
+    for (int h = lane; h < n; h += 32) {
+      d3 x = ld3(s_bh + 3 * h);
       #pragma unroll 1
-      for (uint32_t bb = mask; bb; bb &= bb - 1u) x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
-      st3(tors + 3 * a, x);
+      for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
+        x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
+      st3(torsh + 3 * h, x);
     }
+    hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
+    __syncwarp();
     // initial_poses entry point: the flat centroid of these angles
     // (search.cpp:89-90) instead of flatten's
     if (!ls_mode && A.ang_in) {
       __syncwarp();
-      if (lane < 3) S[S_PIV + lane] = centroid_row(tors, N, lane);
-      __syncwarp();
+      compute_pivot(vb, torsh, S, s_hl, n, N, hx, hv, false, lane);
     }
     // ---- start pose: initial_poses (search.cpp:95-103) or the given one
     if (lane == 0) {
@@ -432,7 +492,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     for (int h = lane; h < n; h += 32) {
       const int a = s_hl[h];
       bool out;
-      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, ld3(tors + 3 * a), a), out);
+      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, ld3(torsh + 3 * h), a), out);
     }
     __syncwarp();
     if (lane == 0) {
@@ -451,7 +511,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       if (lane < 3) S[S_PIV + lane] = centroid_row(A.conf_in + 3 * (size_t)a0, N, lane);
       __syncwarp();
     } else {
-      compute_pivot(vb, tors, S, N, lane);
+      compute_pivot(vb, torsh, S, s_hl, n, N, hx, hv, true, lane);
     }
 
     PH(0)
@@ -472,15 +532,14 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
 #endif
       // rigid neighbour transforms (lanes 0-11)
       if (lane < 12) {
-        double *X = Rj + 16 * lane;
-        if (lane < 6) {  // translations (search.cpp:152-158)
+        if (lane < 6) {  // translations (search.cpp:152-158): rotation stays S_R
           const int axis = lane >> 1;
           const double sign = (lane & 1) ? -1.0 : 1.0;
-          for (int q = 0; q < 9; ++q) X[q] = S[S_R + q];
-          for (int q = 0; q < 3; ++q) X[9 + q] = S[S_T + q];
-          X[9 + axis] = S[S_T + axis] + sign * step_t;
-          for (int q = 0; q < 4; ++q) X[12 + q] = S[S_Q + q];
+          double *X = Tj + 4 * lane;
+          for (int q = 0; q < 3; ++q) X[q] = S[S_T + q];
+          X[axis] = S[S_T + axis] + sign * step_t;
         } else {  // rotations about the pivot (search.cpp:159-167)
+          double *X = Rj + kRow * (lane - 6);
           const double *sq = A.c.spin + 4 * (6 * level + (lane - 6));
           const quat spin{sq[0], sq[1], sq[2], sq[3]};
           const d3 piv = ld3(S + S_PIV);
@@ -489,13 +548,13 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           const quat qn = quat_normalized(quat_mul(spin, cur));  // compose, transform.cpp:18-19
           const d3 tt = add3(quat_rotate(spin, ld3(S + S_T)), spin_t);
           quat_matrix(qn, X);
-          X[9] = tt.x;
-          X[10] = tt.y;
-          X[11] = tt.z;
-          X[12] = qn.x;
-          X[13] = qn.y;
-          X[14] = qn.z;
-          X[15] = qn.w;
+          X[10] = tt.x;
+          X[11] = tt.y;
+          X[12] = tt.z;
+          X[14] = qn.x;
+          X[15] = qn.y;
+          X[16] = qn.z;
+          X[17] = qn.w;
         }
       }
 #ifdef VS_PHASE_PROF
@@ -579,101 +638,70 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           jn = 2 * (thi - tlo);
           items = 2 * (s_doff[thi - 1] + s_dcnt[thi - 1] - s_doff[tlo]);
         }
-        // Rigid and torsion neighbours run in separate compact loops (the hot
-        // code must stay small: the search was instruction-fetch bound).
-        // With kSampleIlp == 2 each lane computes two samples before storing
-        // either, so their load/FP64 latency chains overlap (a store between
-        // them would order the second sample's shared loads after it).
+        // Rigid and torsion neighbours run in separate compact loops, one
+        // sample in flight per lane: the search is instruction-fetch bound
+        // when warps at different phases share an SM (measured: two samples
+        // per lane, even without an intervening store, tripled the
+        // no-instruction stalls), so the hot code is kept small.
         if (grp == 0) {
           // rigid neighbours: lane = heavy atom, loop over the 12 transforms
           // (their matrices are warp-uniform shared-memory broadcasts)
           #pragma unroll 1
           for (int h = lane; h < n; h += 32) {
             const int a = s_hl[h];
-            const d3 x = ld3(tors + 3 * a);
-            if (kSampleIlp == 2) {
-              #pragma unroll 1
-              for (int j = 0; j < 12; j += 2) {
-                bool o0, o1;
-                const double v0 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(Rj + 16 * j, x, a), o0);
-                const double v1 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(Rj + 16 * (j + 1), x, a), o1);
-                vb[j * nmax + h] = v0;
-                vb[(j + 1) * nmax + h] = v1;
-              }
-            } else {
-              #pragma unroll 1
-              for (int j = 0; j < 12; ++j) {
-                bool out;
-                vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(Rj + 16 * j, x, a), out);
-              }
+            const d3 x = ld3(torsh + 3 * h);
+            #pragma unroll 1
+            for (int j = 0; j < 12; ++j) {
+              const double *R = j < 6 ? S + S_R : Rj + kRow * (j - 6);
+              const double *T = j < 6 ? Tj + 4 * j : R + 10;
+              bool out;
+              vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, a), out);
             }
           }
         } else {
-          const uint32_t *ti = s_tit + 2 * s_doff[tlo];
-          if (kSampleIlp == 2) {
-            for (int it = lane; it < items; it += 64) {
-              const bool two = it + 32 < items;
-              const uint32_t e0 = ti[it], e1 = two ? ti[it + 32] : e0;
-              const int v0 = (e0 >> 8) & 63, h0 = e0 & 255, t0 = v0 >> 1;
-              const int v1 = (e1 >> 8) & 63, h1 = e1 & 255, t1 = v1 >> 1;
-              d3 x0 = ld3(s_bh + 3 * h0), x1 = ld3(s_bh + 3 * h1);
-              const uint32_t k0 = s_tmh[h0], k1 = s_tmh[h1];
-              const double *M0 = Mvar + mvar_off(v0, t0, m) - 12 * t0;
-              const double *M1 = Mvar + mvar_off(v1, t1, m) - 12 * t1;
-              #pragma unroll 1
-              for (uint32_t bb = k0 & 0x7fffffffu; bb; bb &= bb - 1u) {
-                const int u = __ffs(bb) - 1;
-                x0 = torsion_apply_a((u < t0 ? Mcur : M0) + 12 * u, x0);
-              }
-              #pragma unroll 1
-              for (uint32_t bb = two ? (k1 & 0x7fffffffu) : 0u; bb; bb &= bb - 1u) {
-                const int u = __ffs(bb) - 1;
-                x1 = torsion_apply_a((u < t1 ? Mcur : M1) + 12 * u, x1);
-              }
-              bool o0, o1;
-              const double f0 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x0, (int)(k0 >> 31)), o0);
-              const double f1 = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x1, (int)(k1 >> 31)), o1);
-              vb[(v0 - 2 * tlo) * nmax + h0] = f0;
-              if (two) vb[(v1 - 2 * tlo) * nmax + h1] = f1;
-            }
-          } else {
+          // item it: (t, h) pair it / 2 of the stored list, sign it & 1
+          const uint32_t *ti = s_tit + s_doff[tlo];
+          #pragma unroll 1
+          for (int it = lane; it < items; it += 32) {
+            const uint32_t e = ti[it >> 1];
+            const int v = ((e >> 8) & 63) | (it & 1), h = e & 255, t = v >> 1;
+            d3 x = ld3(s_bh + 3 * h);
+            const uint32_t mask = s_tmh[h];
+            const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
             #pragma unroll 1
-            for (int it = lane; it < items; it += 32) {
-              const uint32_t e = ti[it];
-              const int v = (e >> 8) & 63, h = e & 255, t = v >> 1;
-              d3 x = ld3(s_bh + 3 * h);
-              const uint32_t mask = s_tmh[h];
-              const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
-              #pragma unroll 1
-              for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
-                const int u = __ffs(bb) - 1;
-                x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
-              }
-              bool out;
-              vb[(v - 2 * tlo) * nmax + h] =
-                  field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x, (int)(mask >> 31)), out);
+            for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
+              const int u = __ffs(bb) - 1;
+              x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
             }
+            bool out;
+            vb[(v - 2 * tlo) * nmax + h] =
+                field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x, (int)(mask >> 31)), out);
+          }
+        }
+        if (grp != 0) {
+          // heavy atoms outside D_t sample exactly as in the current pose:
+          // complete the torsion rows with the current values
+          #pragma unroll 1
+          for (int rr = 0; rr < jn; ++rr) {
+            const int t = tlo + (rr >> 1);
+            #pragma unroll 1
+            for (int h = lane; h < n; h += 32)
+              if (!((s_dm[h] >> t) & 1u)) vb[rr * nmax + h] = vcur[h];
           }
         }
         __syncwarp();
         PH(grp == 0 ? 2 : 3)
         // geo_score of each neighbour in the group (grid.cpp:97-101)
+        double gacc = 0.0;
         if (lane < jn) {
           const double *row = vb + lane * nmax;
           double acc = 0.0;
-          if (grp == 0) {
-            #pragma unroll 4
-            for (int h = 0; h < n; ++h) acc += row[h];
-          } else {
-            const int t = tlo + (lane >> 1);
-            #pragma unroll 4
-            for (int h = 0; h < n; ++h) acc += ((s_dm[h] >> t) & 1u) ? row[h] : vcur[h];
-          }
-          scores[lane] = acc;
+          #pragma unroll 4
+          for (int h = 0; h < n; ++h) acc += row[h];
+          gacc = acc;
         }
-        __syncwarp();
         // first strict maximum of the group, then against the running best
-        double gv = lane < jn ? scores[lane] : -__longlong_as_double(0x7ff0000000000000LL);
+        double gv = lane < jn ? gacc : -__longlong_as_double(0x7ff0000000000000LL);
         int gj = lane < jn ? lane : 0x7fffffff;
         for (int off = 16; off > 0; off >>= 1) {
           const double ov = __shfl_xor_sync(0xffffffffu, gv, off);
@@ -687,14 +715,8 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           bv = gv;
           bj = j0 + gj;
           const double *row = vb + gj * nmax;
-          if (grp == 0) {
-            #pragma unroll 1
-            for (int h = lane; h < n; h += 32) vbest[h] = row[h];
-          } else {
-            const int t = tlo + (gj >> 1);
-            #pragma unroll 1
-            for (int h = lane; h < n; h += 32) vbest[h] = ((s_dm[h] >> t) & 1u) ? row[h] : vcur[h];
-          }
+          #pragma unroll 1
+          for (int h = lane; h < n; h += 32) vbest[h] = row[h];
         }
         __syncwarp();
         PH(4)
@@ -704,11 +726,13 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       if (bj >= 0) {
         ++n_adopt;
         moved = true;
-        if (bj < 12) {
-          const double *X = Rj + 16 * bj;
+        if (bj < 6) {
+          if (lane < 3) S[S_T + lane] = Tj[4 * bj + lane];
+        } else if (bj < 12) {
+          const double *X = Rj + kRow * (bj - 6);
           if (lane < 9) S[S_R + lane] = X[lane];
-          else if (lane < 12) S[S_T + lane - 9] = X[lane];
-          else if (lane < 16) S[S_Q + lane - 12] = X[lane];
+          else if (lane < 12) S[S_T + lane - 9] = X[lane + 1];
+          else if (lane < 16) S[S_Q + lane - 12] = X[lane + 2];
         } else {
           const int v = bj - 12, t = v >> 1;
           const double sign = (v & 1) ? -1.0 : 1.0;
@@ -726,20 +750,21 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           chain_from = t;
           __syncwarp();
           #pragma unroll 1
-          for (int a = lane; a < N; a += 32) {
-            d3 x = ld3(base + 3 * a);
-            const uint32_t mask = tm[a];
+          for (int h = lane; h < n; h += 32) {
+            d3 x = ld3(s_bh + 3 * h);
             #pragma unroll 1
-            for (uint32_t bb = mask; bb; bb &= bb - 1u) x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
-            st3(tors + 3 * a, x);
+            for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
+              x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
+            st3(torsh + 3 * h, x);
           }
+          hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
         }
         #pragma unroll 1
         for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
         if (lane == 0) S[S_GEO] = bv;
         __syncwarp();
         // new pivot = centroid of the adopted conformation (vb is free here)
-        compute_pivot(vb, tors, S, N, lane);
+        compute_pivot(vb, torsh, S, s_hl, n, N, hx, hv, true, lane);
         PH(bj < 12 ? 5 : 6)
       } else {
         if (lane == 0) {
@@ -767,9 +792,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       #pragma unroll 1
       for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
     } else {
-      #pragma unroll 1
-      for (int a = lane; a < N; a += 32)
-        st3(A.o.conf + ck + 3 * a, rigid_col_a(S + S_R, ld3(tors + 3 * a), a));
+      full_conformation(A.o.conf + ck, torsh, S, s_hl, n, N, hx, hv, true, lane);
     }
     const size_t tk = (size_t)t0 * k + (size_t)r * m;
     #pragma unroll 1
@@ -795,13 +818,13 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
 namespace {
 
 struct Layout {
-  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_scores, o_cache, o_ang, o_sccur, o_state, o_ints, total;
+  int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_cache, o_ang, o_sccur, o_state, o_ints, total;
   int cta;  // CTA-shared ligand staging, doubles
 };
 
 Layout layout(int Nm, int nm, int mm, int dm) {
   Layout L{};
-  L.cta = 3 * nm + 6 * mm + (3 * nm + 4 * mm + 2 * dm + 1) / 2 + 1;
+  L.cta = 3 * nm + 6 * mm + (3 * nm + 4 * mm + dm + 1) / 2 + 1;
   L.cta = (L.cta + 1) & ~1;
   int o = 0;
   auto take = [&](int n) {
@@ -809,14 +832,13 @@ Layout layout(int Nm, int nm, int mm, int dm) {
     o += (n + 1) & ~1;  // keep 16-byte alignment
     return at;
   };
-  L.o_tors = take(3 * Nm);
+  L.o_tors = take(3 * nm);
   L.o_Mcur = take(12 * mm);
   L.o_Mvar = take(12 * mm * (mm + 1));
-  L.o_Rj = take(16 * 12);
+  L.o_Rj = take(kRow * 6 + 4 * 6);
   L.o_vb = take(kGroup * nm > 3 * Nm ? kGroup * nm : 3 * Nm);  // also the pivot scratch
   L.o_vbest = take(nm);
   L.o_vcur = take(nm);
-  L.o_scores = take(kGroup);
   L.o_cache = take(8 * mm);  // sin/cos of the 2m variant angles: hi parts, then lo parts
   L.o_ang = take(mm);
   L.o_sccur = take(4 * mm);  // sin/cos of the current angles: hi parts, then lo parts
@@ -836,7 +858,6 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   A.o_vb = L.o_vb;
   A.o_vbest = L.o_vbest;
   A.o_vcur = L.o_vcur;
-  A.o_scores = L.o_scores;
   A.o_cache = L.o_cache;
   A.o_ang = L.o_ang;
   A.o_sccur = L.o_sccur;
@@ -890,7 +911,10 @@ extern "C" int vs_debug_phase_read(unsigned long long *out, int reset) {
 }
 #endif
 
-size_t search_args_bytes() { return sizeof(search_args); }
+// Global scratch of the search: one hydrogen frame per resident warp.
+size_t search_scratch_bytes(int nmax_atoms, int num_sms) {
+  return (size_t)num_sms * 16 * 3 * (size_t)(nmax_atoms > 0 ? nmax_atoms : 1) * sizeof(double);
+}
 
 int search_warps_per_cta() { return kWarps; }
 
@@ -903,8 +927,8 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf, const int *lig_index,
                           int n_lig, int dmax) {
-  (void)args_buf;
   search_args A{};
+  A.hscr = static_cast<double *>(args_buf);
   A.b = b;
   A.p = p;
   A.pg = p.packed;
@@ -925,8 +949,8 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
 cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const double *angles,
                                  const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                                  int num_sms, cudaStream_t s, void *args_buf) {
-  (void)args_buf;
   search_args A{};
+  A.hscr = static_cast<double *>(args_buf);
   A.b = b;
   A.p = p;
   A.pg = p.packed;
@@ -948,8 +972,8 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
                                 const double *ang_in, const double *conf_in, const item_out &o, int *work_counter,
                                 int nmax_atoms, int nmax_heavy, int mmax, int num_sms, cudaStream_t s,
                                 void *args_buf) {
-  (void)args_buf;
   search_args A{};
+  A.hscr = static_cast<double *>(args_buf);
   A.b = b;
   A.p = p;
   A.pg = p.packed;
