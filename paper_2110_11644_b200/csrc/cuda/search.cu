@@ -135,15 +135,15 @@ __device__ __forceinline__ double c_lattice_sc_dev(int i) { return c_lattice_sc_
 
 enum {
   S_Q = 0,      // current rotation (x, y, z, w)
-  S_R = 4,      // current rotation matrix (16-byte aligned, translation follows:
-  S_T = 13,     //   R and t load as one 12-double block, like the Rj rows)
-  S_PIV = 16,   // pivot
-  S_GEO = 19,   // current geo_score
-  S_STEPT = 20,
-  S_STEPR = 21,
-  S_STEPQ = 22,
-  S_ERR = 23,
-  S_N = 24
+  S_R = 4,      // current rotation matrix (16-byte aligned)
+  S_T = 14,     // current translation (16-byte aligned)
+  S_PIV = 17,   // pivot
+  S_GEO = 20,   // current geo_score
+  S_STEPT = 21,
+  S_STEPR = 22,
+  S_STEPQ = 23,
+  S_ERR = 24,
+  S_N = 25
 };
 
 }  // namespace
@@ -282,13 +282,13 @@ __device__ __noinline__ void full_conformation(double *out, const double *torsh,
   for (int h = lane; h < n; h += 32) {
     const int a = hl[h];
     const d3 x = ld3(torsh + 3 * h);
-    st3(out + 3 * a, rigid ? rigid_col_a(S + S_R, x, a) : x);
+    st3(out + 3 * a, rigid ? rigid_col_rt(S + S_R, S + S_T, x, a) : x);
   }
   #pragma unroll 1
   for (int a = lane; a < N; a += 32) {
     if (heavy[a]) continue;
     const d3 x = ld3(hx + 3 * a);
-    st3(out + 3 * a, rigid ? rigid_col_a(S + S_R, x, a) : x);
+    st3(out + 3 * a, rigid ? rigid_col_rt(S + S_R, S + S_T, x, a) : x);
   }
 }
 
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     for (int h = lane; h < n; h += 32) {
       const int a = s_hl[h];
       bool out;
-      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, ld3(torsh + 3 * h), a), out);
+      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(S + S_R, S + S_T, ld3(torsh + 3 * h), a), out);
     }
     __syncwarp();
     if (lane == 0) {
@@ -643,39 +643,60 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         // when warps at different phases share an SM (measured: two samples
         // per lane, even without an intervening store, tripled the
         // no-instruction stalls), so the hot code is kept small.
-        if (grp == 0) {
-          // rigid neighbours: lane = heavy atom, loop over the 12 transforms
-          // (their matrices are warp-uniform shared-memory broadcasts)
-          #pragma unroll 1
-          for (int h = lane; h < n; h += 32) {
-            const int a = s_hl[h];
-            const d3 x = ld3(torsh + 3 * h);
+        // One sample loop for both kinds of group (the hot code must stay
+        // small: the search is instruction-fetch bound when warps at
+        // different phases share an SM).  Rigid item it = (transform j, heavy
+        // atom h), walked incrementally; torsion item it = (t, h) pair it / 2
+        // of the stored list with sign it & 1, its chain from the base
+        // coordinates through the current / the variant's matrices.
+        {
+          const bool rig = grp == 0;
+          const uint32_t *ti = s_tit + s_doff[tlo];
+          int rj = 0, rh = lane;
+          if (rig && n > 0) {  // (n == 0: a hydrogen-only ligand docked with k == 1 has no items)
             #pragma unroll 1
-            for (int j = 0; j < 12; ++j) {
-              const double *R = j < 6 ? S + S_R : Rj + kRow * (j - 6);
-              const double *T = j < 6 ? Tj + 4 * j : R + 10;
-              bool out;
-              vb[j * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, a), out);
+            while (rh >= n) {
+              rh -= n;
+              ++rj;
             }
           }
-        } else {
-          // item it: (t, h) pair it / 2 of the stored list, sign it & 1
-          const uint32_t *ti = s_tit + s_doff[tlo];
           #pragma unroll 1
           for (int it = lane; it < items; it += 32) {
-            const uint32_t e = ti[it >> 1];
-            const int v = ((e >> 8) & 63) | (it & 1), h = e & 255, t = v >> 1;
-            d3 x = ld3(s_bh + 3 * h);
-            const uint32_t mask = s_tmh[h];
-            const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
-            #pragma unroll 1
-            for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
-              const int u = __ffs(bb) - 1;
-              x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
+            int row, h, col;
+            const double *R, *T;
+            d3 x;
+            if (rig) {
+              h = rh;
+              row = rj;
+              col = s_hl[h];
+              R = rj < 6 ? S + S_R : Rj + kRow * (rj - 6);
+              T = rj < 6 ? Tj + 4 * rj : R + 10;
+              x = ld3(torsh + 3 * h);
+              rh += 32;
+              #pragma unroll 1
+              while (rh >= n) {
+                rh -= n;
+                ++rj;
+              }
+            } else {
+              const uint32_t e = ti[it >> 1];
+              const int v = ((e >> 8) & 63) | (it & 1), t = v >> 1;
+              h = e & 255;
+              x = ld3(s_bh + 3 * h);
+              const uint32_t mask = s_tmh[h];
+              col = (int)(mask >> 31);
+              const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
+              #pragma unroll 1
+              for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
+                const int u = __ffs(bb) - 1;
+                x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
+              }
+              row = v - 2 * tlo;
+              R = S + S_R;
+              T = S + S_T;
             }
             bool out;
-            vb[(v - 2 * tlo) * nmax + h] =
-                field_value_fast<MODE>(g, pg, pal, rigid_col_a(S + S_R, x, (int)(mask >> 31)), out);
+            vb[row * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, col), out);
           }
         }
         if (grp != 0) {
