@@ -814,7 +814,7 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
     if ((rc = flatten_buckets(ctx, st, cfg->flatten_max_sweeps, f))) return rc;
     CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
-    CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), ctx->num_sms)));
+    CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), std::max(st.nmax, 1), std::max(st.mmax, 1), ctx->num_sms)));
     CUDA_TRY(cudaEventSynchronize(ctx->ev1));
     {
       // Size buckets: ligands grouped by how many 4-warp search CTAs per SM
@@ -989,7 +989,7 @@ vs_status vs_initial_poses(vs_context *ctx, const vs_pocket *pocket, const vs_li
   if ((rc = ensure_items(ctx, st, k, o))) return rc;
   CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
   CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
-  CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), ctx->num_sms)));
+  CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), std::max(st.nmax, 1), std::max(st.mmax, 1), ctx->num_sms)));
   CUDA_TRY(vsd::launch_initial_poses(st.b, pocket->dev(), sc, ctx->aux1.as<double>(), o, ctx->work.as<int>(), st.Nmax,
                                      st.nmax, st.mmax, ctx->num_sms, ctx->stream, ctx->search_args.p));
   std::vector<double> T(static_cast<size_t>(7) * k), geo(static_cast<size_t>(k));
@@ -1074,7 +1074,7 @@ vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const 
   if ((rc = ensure_items(ctx, st, 1, o))) return rc;
   CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
   CUDA_TRY(vsd::launch_setup(st.b, 1, ctx->stream));
-  CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), ctx->num_sms)));
+  CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), std::max(st.nmax, 1), std::max(st.mmax, 1), ctx->num_sms)));
   CUDA_TRY(vsd::launch_local_search(st.b, pocket->dev(), sc, ctx->aux0.as<double>(), ctx->aux1.as<double>(),
                                     ctx->aux2.as<double>(), o, ctx->work.as<int>(), st.Nmax, st.nmax, st.mmax,
                                     ctx->num_sms, ctx->stream, ctx->search_args.p));

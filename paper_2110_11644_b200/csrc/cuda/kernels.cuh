@@ -116,7 +116,7 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
                           int num_sms, cudaStream_t s, int *launches, void *args_buf,
                           const int *lig_index = nullptr, int n_lig = 0, int dmax = 0);
 // device buffer size the search launchers need for their argument block
-size_t search_scratch_bytes(int nmax_atoms, int num_sms);
+size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms);
 // dynamic shared memory of one k_search CTA for the given ligand maxima
 size_t search_smem_bytes(int N, int n, int m, int dtot);
 int search_warps_per_cta();

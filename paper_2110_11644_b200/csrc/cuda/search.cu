@@ -71,11 +71,6 @@ __device__ __forceinline__ d3 torsion_apply_a(const double *m, d3 x) {
   ld12a(m, r);
   return torsion_apply(r, x);
 }
-__device__ __forceinline__ d3 rigid_col_a(const double *rt, d3 v, int col) {
-  double r[12];
-  ld12a(rt, r);
-  return rigid_col(r, r + 9, v, col);
-}
 // Rotation (9 doubles) and translation (3) at two 16-byte aligned addresses.
 __device__ __forceinline__ d3 rigid_col_rt(const double *R, const double *T, d3 v, int col) {
   double r[9], t[3];
@@ -272,6 +267,25 @@ __device__ __noinline__ void hydrogen_frame(double *hx, int N, const double *bas
   }
 }
 
+// Stage-t prefix positions of the torsion items (search.cpp:168-176): pair p
+// = (t, h in D_t) of the stored list gets h's base coordinates carried
+// through the current matrices of torsions u < t (the part of its chain that
+// is the same for (t,+) and (t,-) and for every step level), pairs from
+// `pfrom` on.  Recomputed only when a torsion move changes Mcur.
+__device__ __noinline__ void prefix_frame(double *pc, const uint32_t *tit, int pfrom, int npairs, const double *bh,
+                                          const uint32_t *tmh, const double *Mcur, int lane) {
+  #pragma unroll 1
+  for (int p = pfrom + lane; p < npairs; p += 32) {
+    const uint32_t e = tit[p];
+    const int h = e & 255, t = (e >> 9) & 31;
+    d3 x = ld3(bh + 3 * h);
+    #pragma unroll 1
+    for (uint32_t bb = tmh[h] & ((1u << t) - 1u); bb; bb &= bb - 1u)
+      x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
+    st3(pc + 3 * p, x);
+  }
+}
+
 // The whole conformation of the current pose into `out` (3N, atom order):
 // heavy atoms from the shared-memory frame `torsh`, hydrogens from `hx`,
 // then apply_rigid (transform.cpp:31) when `rigid`.
@@ -325,7 +339,10 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   __shared__ int sh_lig, sh_r;
   double *W = sm + 16 + A.cta_doubles + (size_t)warp * A.warp_doubles;
   double *torsh = W + A.o_tors;  // 3 * nmax: torsioned frame of the heavy atoms (search.cpp:115)
-  double *hx = A.hscr + (size_t)(blockIdx.x * kWarps + warp) * 3 * A.Nmax;  // hydrogens' frame (global)
+  // per-warp global scratch: the hydrogens' torsioned frame (3 * Nmax) and
+  // the stage-t prefix positions of the torsion items (3 * nmax * mmax)
+  double *hx = A.hscr + (size_t)(blockIdx.x * kWarps + warp) * 3 * (A.Nmax + A.nmax * A.mmax);
+  double *pc = hx + 3 * A.Nmax;
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
   double *Rj = W + A.o_Rj;       // 6 spin neighbours x kRow: R at 0, t at 10, q at 14 (16-byte aligned)
@@ -450,6 +467,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       st3(torsh + 3 * h, x);
     }
     hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
+    prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane);
     __syncwarp();
     // initial_poses entry point: the flat centroid of these angles
     // (search.cpp:89-90) instead of flatten's
@@ -652,6 +670,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         {
           const bool rig = grp == 0;
           const uint32_t *ti = s_tit + s_doff[tlo];
+          const double *pcg = pc + 3 * s_doff[tlo];
           int rj = 0, rh = lane;
           if (rig && n > 0) {  // (n == 0: a hydrogen-only ligand docked with k == 1 has no items)
             #pragma unroll 1
@@ -682,15 +701,13 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
               const uint32_t e = ti[it >> 1];
               const int v = ((e >> 8) & 63) | (it & 1), t = v >> 1;
               h = e & 255;
-              x = ld3(s_bh + 3 * h);
+              x = ld3(pcg + 3 * (it >> 1));  // stage-t prefix (prefix_frame)
               const uint32_t mask = s_tmh[h];
               col = (int)(mask >> 31);
               const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
               #pragma unroll 1
-              for (uint32_t bb = mask & 0x7fffffffu; bb; bb &= bb - 1u) {
-                const int u = __ffs(bb) - 1;
-                x = torsion_apply_a((u < t ? Mcur : Mv) + 12 * u, x);
-              }
+              for (uint32_t bb = (mask & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u)
+                x = torsion_apply_a(Mv + 12 * (__ffs(bb) - 1), x);
               row = v - 2 * tlo;
               R = S + S_R;
               T = S + S_T;
@@ -779,6 +796,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             st3(torsh + 3 * h, x);
           }
           hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
+          prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane);
         }
         #pragma unroll 1
         for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
@@ -932,9 +950,11 @@ extern "C" int vs_debug_phase_read(unsigned long long *out, int reset) {
 }
 #endif
 
-// Global scratch of the search: one hydrogen frame per resident warp.
-size_t search_scratch_bytes(int nmax_atoms, int num_sms) {
-  return (size_t)num_sms * 16 * 3 * (size_t)(nmax_atoms > 0 ? nmax_atoms : 1) * sizeof(double);
+// Global scratch of the search per resident warp: hydrogen frame and the
+// torsion items' prefix positions.
+size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms) {
+  const size_t N = nmax_atoms > 0 ? nmax_atoms : 1, n = nmax_heavy > 0 ? nmax_heavy : 1, m = mmax > 0 ? mmax : 1;
+  return (size_t)num_sms * 16 * 3 * (N + n * m) * sizeof(double);
 }
 
 int search_warps_per_cta() { return kWarps; }
