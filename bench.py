@@ -157,6 +157,18 @@ def split_flops(counters: np.ndarray, batch, k: int) -> dict:
     return {"search": float(search.sum()), "flatten": float(flatten.sum()), "select": float(select.sum())}
 
 
+def traffic_per_launch(n_ligands: int):
+    """DRAM bytes of the search stage for one step: the per-ligand figure of
+    the committed ncu capture (profiles/r01_traffic.json, dram__bytes_read +
+    dram__bytes_write of one k_search launch) times the step's ligands."""
+    path = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["dram_bytes_per_ligand"]) * n_ligands
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def measure_fp64_peak(device: int) -> dict:
     from paper_2110_11644_b200 import native
     import ctypes as C
@@ -348,7 +360,8 @@ def main():
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world},
         "gpu_launches": launches,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic_per_launch(batch.n_ligands),
+                     "traffic_unit": "bytes (DRAM read + write of the search stage of one step, ncu)",
                      "kernel": "k_search (initial_poses + local_search)",
                      "flops_per_launch": fl["search"], "launch_ms": st_last["search"],
                      "peak_source": "measured live: FP64 DADD/DMUL issue rate (no FMA: -fmad=false)",
