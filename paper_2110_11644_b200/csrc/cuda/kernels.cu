@@ -536,11 +536,167 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   }
 }
 
+// The same for k <= 32 restarts with one warp per ligand (lane = restart /
+// leader / survivor): no CTA barriers, 4 independent ligands per CTA.
+constexpr int kSelWarps = 4;
+
+__global__ void __launch_bounds__(32 * kSelWarps) k_select_warp(batch_dev b, pocket_dev p, search_cfg c, item_out o,
+                                                               dock_out d) {
+  __shared__ int s_order[kSelWarps][32], s_lead[kSelWarps][32], s_foll[kSelWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int l = blockIdx.x * kSelWarps + w;
+  if (l >= b.n_lig) return;
+  const int k = c.k;
+  int *order = s_order[w], *leaders = s_lead[w], *followers = s_foll[w];
+  vs_dock_result *res = reinterpret_cast<vs_dock_result *>(d.results) + l;
+  const lig_meta meta = b.meta[l];
+  int status = meta.status;
+  if (status == VS_LIG_OK) {
+    const int st = lane < k ? o.status[(size_t)l * k + lane] : VS_LIG_OK;
+    status = __reduce_max_sync(0xffffffffu, st);
+  }
+  if (status != VS_LIG_OK) {
+    if (lane == 0) {
+      vs_dock_result z{};
+      z.status = status;
+      *res = z;
+    }
+    return;
+  }
+  const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
+  const int a0 = b.atom_off[l], t0 = b.tors_off[l];
+  const uint16_t *hl = b.heavy_list + a0;
+  const double *geo = o.geo + (size_t)l * k;
+  const double *confs = o.conf + 3 * (size_t)a0 * k;  // pose r at + 3*r*N
+  // stable sort by descending geo_score (search.cpp:201-206)
+  if (lane < k) {
+    const double gi = geo[lane];
+    int rank = 0;
+    for (int j = 0; j < k; ++j) {
+      const double gj = geo[j];
+      rank += (gj > gi || (gj == gi && j < lane)) ? 1 : 0;
+    }
+    order[rank] = lane;
+  }
+  __syncwarp();
+  // greedy leader clustering (search.cpp:208-223): lane li tests leader li
+  int n_lead = 0, n_follow = 0;
+  unsigned long long rmsd_terms = 0ull;
+  #pragma unroll 1
+  for (int vi = 0; vi < k; ++vi) {
+    const int idx = order[vi];
+    const double *ci = confs + 3 * (size_t)idx * N;
+    bool match = false;
+    if (lane < n_lead) {
+      const double *cl = confs + 3 * (size_t)leaders[lane] * N;
+      double sum = 0.0;
+      #pragma unroll 1
+      for (int h = 0; h < n; ++h) {
+        const int a = hl[h];
+        sum += sqn3(sub3(ld3(ci + 3 * a), ld3(cl + 3 * a)));
+      }
+      match = dsqrt(sum / (double)n) <= c.rmsd_threshold;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, match);
+    // the reference stops at the first leader within threshold
+    rmsd_terms += (unsigned long long)n * (bal ? (unsigned)__ffs(bal) : (unsigned)n_lead);
+    if (lane == 0) {
+      if (bal)
+        followers[n_follow] = idx;
+      else
+        leaders[n_lead] = idx;
+    }
+    if (bal) ++n_follow;
+    else ++n_lead;
+    __syncwarp();
+  }
+  const int top = c.rescored < k ? c.rescored : k;
+  // survivors: leaders then followers, truncated (search.cpp:225-235)
+  double chem = -__longlong_as_double(0x7ff0000000000000LL);
+  int clash = 0, pairs = 0;
+  if (lane < top) {
+    const int idx = lane < n_lead ? leaders[lane] : followers[lane - n_lead];
+    chem = chem_pose(p, confs + 3 * (size_t)idx * N, hl, b.elem + a0, n, clash, pairs);
+  }
+  // strict argmax, first survivor on ties (search.cpp:255-265); NaN never
+  // beats anything, as in the sequential `chem > best` scan
+  double bc = isnan(chem) ? -__longlong_as_double(0x7ff0000000000000LL) : chem;
+  int bs = lane < top ? lane : 0x7fffffff;
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bc, off);
+    const int os = __shfl_xor_sync(0xffffffffu, bs, off);
+    if (ov > bc || (ov == bc && os < bs)) {
+      bc = ov;
+      bs = os;
+    }
+  }
+  if (!(bc > -__longlong_as_double(0x7ff0000000000000LL))) bs = 0;  // all -inf/nan: the first survivor
+  const int best_clash = __shfl_sync(0xffffffffu, clash, bs & 31);
+  const double best = __shfl_sync(0xffffffffu, chem, bs & 31);
+  unsigned long long pchem = lane < top ? (unsigned long long)pairs : 0ull;
+  for (int off = 16; off > 0; off >>= 1) pchem += __shfl_xor_sync(0xffffffffu, pchem, off);
+  const int bidx = bs < n_lead ? leaders[bs] : followers[bs - n_lead];
+  const double *bconf = confs + 3 * (size_t)bidx * N;
+  if (d.best_conf)
+    for (int i = lane; i < 3 * N; i += 32) d.best_conf[3 * (size_t)a0 + i] = bconf[i];
+  if (d.best_ang)
+    for (int u = lane; u < m; u += 32) d.best_ang[t0 + u] = o.ang[(size_t)t0 * k + (size_t)bidx * m + u];
+  int oob = 0;
+  for (int h = lane; h < n; h += 32) {
+    bool out;
+    field_value(p.g, ld3(bconf + 3 * hl[h]), out);
+    oob += out ? 1 : 0;
+  }
+  oob = __reduce_add_sync(0xffffffffu, oob);
+  unsigned long long ev = lane < k ? o.evals[(size_t)l * k + lane] : 0ull;
+  unsigned long long iters = lane < k && o.iters ? (unsigned long long)o.iters[(size_t)l * k + lane] : 0ull;
+  unsigned long long adopts = lane < k && o.adopts ? (unsigned long long)o.adopts[(size_t)l * k + lane] : 0ull;
+  for (int off = 16; off > 0; off >>= 1) {
+    ev += __shfl_xor_sync(0xffffffffu, ev, off);
+    iters += __shfl_xor_sync(0xffffffffu, iters, off);
+    adopts += __shfl_xor_sync(0xffffffffu, adopts, off);
+  }
+  if (lane == 0) {
+    vs_dock_result rr{};
+    rr.status = isfinite(best) ? VS_LIG_OK : VS_LIG_NONFINITE;
+    rr.n_survivors = top;
+    rr.best_score = best;
+    const size_t item = (size_t)l * k + bidx;
+    rr.best_geo_score = o.geo[item];
+    for (int q = 0; q < 4; ++q) rr.rotation[q] = o.T[7 * item + q];
+    for (int q = 0; q < 3; ++q) rr.translation[q] = o.T[7 * item + 4 + q];
+    rr.poses_evaluated = (uint64_t)k;
+    rr.scoring_evals = ev;
+    rr.clash_pairs = best_clash;
+    rr.oob_samples = oob;
+    *res = rr;
+    if (d.counters) {
+      // Appendix B counter model, reproduced from the run's integers.
+      const unsigned long long NN = N, nn = n, mm = m, kk = k, J = 12 + 2 * mm;
+      const unsigned long long cand = 36ull * mm * (unsigned long long)f_sweeps_of(d, l);
+      unsigned long long *cn = d.counters + 9 * (size_t)l;
+      cn[0] = ev;
+      cn[1] = kk * NN + iters * J * nn + adopts * NN;
+      cn[2] = cand * (unsigned long long)meta.r_all + iters * 2ull * mm * (unsigned long long)meta.r_heavy;
+      cn[3] = cand * mm + 2ull * mm + kk * mm + iters * 2ull * mm * mm;
+      cn[4] = cand * (NN * (NN - 1) / 2);
+      cn[5] = pchem;
+      cn[6] = rmsd_terms;
+      cn[7] = (unsigned long long)best_clash;
+      cn[8] = (unsigned long long)oob;
+    }
+  }
+}
+
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s) {
   (void)nmax_atoms;
   if (b.n_lig == 0) return cudaSuccess;
   const int k = c.k;
+  if (k <= 32) {
+    k_select_warp<<<(b.n_lig + kSelWarps - 1) / kSelWarps, 32 * kSelWarps, 0, s>>>(b, p, c, o, d);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + 2 * sizeof(int) * k + 16;
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d);
