@@ -43,6 +43,7 @@ constexpr int kWarps = VS_SEARCH_WARPS;
 #ifndef VS_SEARCH_GROUP
 #define VS_SEARCH_GROUP 12
 #endif
+constexpr int kPalDoubles = 32;  // palette / code-pair table at the start of shared memory
 constexpr int kRow = 18;  // spin-neighbour row: R (9), pad, t (3), pad, q (4)
 constexpr int kGroup = VS_SEARCH_GROUP;  // neighbours per group (>= 12, even; 12 measured best)
 constexpr double kPi = 3.14159265358979323846;
@@ -321,13 +322,19 @@ __device__ __forceinline__ void compute_pivot(double *scratch, const double *tor
 template <int MODE>
 __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args A) {
   extern __shared__ __align__(16) double sm[];
-  double *pal = sm;  // 16 palette values (CTA-wide)
+  // palette (CTA-wide): MODE 2 reads the 16 values; MODE 1 a table of code
+  // pairs, entry i = (palette[i & 3], palette[i >> 2]), so two corners of a
+  // cell come with one 128-bit load
+  double *pal = sm;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  if (threadIdx.x < 16) pal[threadIdx.x] = MODE == 0 ? 0.0 : A.p.palette[threadIdx.x];
+  if (threadIdx.x < kPalDoubles)
+    pal[threadIdx.x] = MODE == 0 ? 0.0
+                       : MODE == 1 ? A.p.palette[(threadIdx.x & 1) ? ((threadIdx.x >> 1) >> 2) : ((threadIdx.x >> 1) & 3)]
+                                   : (threadIdx.x < 16 ? A.p.palette[threadIdx.x] : 0.0);
   // CTA-shared staging of the current ligand (all warps of the CTA run its
   // restarts): heavy-atom base coordinates, torsion endpoints, masks, items
-  double *s_bh = sm + 16;                 // 3 * nmax: base coordinates of heavy atom h
+  double *s_bh = sm + kPalDoubles;        // 3 * nmax: base coordinates of heavy atom h
   double *s_ep = s_bh + 3 * A.nmax;       // 6 * mmax: base coordinates of torsion u's endpoints
   uint32_t *s_tmh = reinterpret_cast<uint32_t *>(s_ep + 6 * A.mmax);  // nmax: torsion mask | parity << 31
   uint32_t *s_dm = s_tmh + A.nmax;        // nmax: D_t membership of heavy atom h
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   int *s_dcnt = s_doff + A.mmax;          // mmax
   uint32_t *s_tit = reinterpret_cast<uint32_t *>(s_dcnt + A.mmax);  // dmax: (t, h in D_t) pairs, h | 2t << 8
   __shared__ int sh_lig, sh_r;
-  double *W = sm + 16 + A.cta_doubles + (size_t)warp * A.warp_doubles;
+  double *W = sm + kPalDoubles + A.cta_doubles + (size_t)warp * A.warp_doubles;
   double *torsh = W + A.o_tors;  // 3 * nmax: torsioned frame of the heavy atoms (search.cpp:115)
   // per-warp global scratch: the hydrogens' torsioned frame (3 * Nmax) and
   // the stage-t prefix positions of the torsion items (3 * nmax * mmax)
@@ -904,7 +911,7 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   A.o_ints = L.o_ints;
   A.warp_doubles = L.total;
   const int o = L.total;
-  const size_t smem = (size_t)(16 + L.cta + o * kWarps) * sizeof(double);
+  const size_t smem = (size_t)(kPalDoubles + L.cta + o * kWarps) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const void *fn = A.pg.mode == 1 ? (const void *)k_search<1>
                                   : (A.pg.mode == 2 ? (const void *)k_search<2> : (const void *)k_search<0>);
@@ -961,7 +968,7 @@ int search_warps_per_cta() { return kWarps; }
 
 size_t search_smem_bytes(int N, int n, int m, int dtot) {
   const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1, dtot > 0 ? dtot : 1);
-  return (size_t)(16 + L.cta + L.total * kWarps) * sizeof(double);
+  return (size_t)(kPalDoubles + L.cta + L.total * kWarps) * sizeof(double);
 }
 
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
