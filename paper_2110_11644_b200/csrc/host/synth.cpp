@@ -142,7 +142,9 @@ extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, 
       auto &out = blocks[static_cast<size_t>(bi)];
       int64_t tries = 0;
       while (static_cast<int>(out.size()) < want) {
-        if (++tries > 20000LL * kBlock) {
+        // give up on windows the grammar cannot reach (nothing accepted in
+        // 200k candidates) or reaches too rarely
+        if (++tries > 4000LL * kBlock || (out.empty() && tries > 200000) || unreachable) {
           unreachable = true;
           return;
         }
