@@ -288,20 +288,12 @@ __device__ __noinline__ void prefix_frame(double *pc, const uint32_t *tit, int p
 }
 
 // The whole conformation of the current pose into `out` (3N, atom order):
-// heavy atoms from the shared-memory frame `torsh`, hydrogens from `hx`,
-// then apply_rigid (transform.cpp:31) when `rigid`.
-__device__ __noinline__ void full_conformation(double *out, const double *torsh, const double *S, const uint32_t *hl,
-                                               int n, int N, const double *hx, const uint8_t *heavy, bool rigid,
+// the torsioned frame `hx` (global scratch, every atom), then apply_rigid
+// (transform.cpp:31) when `rigid`.
+__device__ __noinline__ void full_conformation(double *out, const double *S, int N, const double *hx, bool rigid,
                                                int lane) {
   #pragma unroll 1
-  for (int h = lane; h < n; h += 32) {
-    const int a = hl[h];
-    const d3 x = ld3(torsh + 3 * h);
-    st3(out + 3 * a, rigid ? rigid_col_rt(S + S_R, S + S_T, x, a) : x);
-  }
-  #pragma unroll 1
   for (int a = lane; a < N; a += 32) {
-    if (heavy[a]) continue;
     const d3 x = ld3(hx + 3 * a);
     st3(out + 3 * a, rigid ? rigid_col_rt(S + S_R, S + S_T, x, a) : x);
   }
@@ -310,10 +302,9 @@ __device__ __noinline__ void full_conformation(double *out, const double *torsh,
 // Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
 // the transformed conformation to `scratch`, then three lanes run the
 // Eigen-order row sums (dmath.cuh centroid_row).
-__device__ __forceinline__ void compute_pivot(double *scratch, const double *torsh, double *S, const uint32_t *hl,
-                                              int n, int N, const double *hx, const uint8_t *heavy, bool rigid,
+__device__ __forceinline__ void compute_pivot(double *scratch, double *S, int N, const double *hx, bool rigid,
                                               int lane) {
-  full_conformation(scratch, torsh, S, hl, n, N, hx, heavy, rigid, lane);
+  full_conformation(scratch, S, N, hx, rigid, lane);
   __syncwarp();
   if (lane < 3) S[S_PIV + lane] = centroid_row(scratch, N, lane);
   __syncwarp();
@@ -472,6 +463,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
         x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
       st3(torsh + 3 * h, x);
+      st3(hx + 3 * s_hl[h], x);  // every atom's frame also in hx (pivots, outputs)
     }
     hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
     prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane);
@@ -480,7 +472,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     // (search.cpp:89-90) instead of flatten's
     if (!ls_mode && A.ang_in) {
       __syncwarp();
-      compute_pivot(vb, torsh, S, s_hl, n, N, hx, hv, false, lane);
+      compute_pivot(vb, S, N, hx, false, lane);
     }
     // ---- start pose: initial_poses (search.cpp:95-103) or the given one
     if (lane == 0) {
@@ -536,7 +528,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       if (lane < 3) S[S_PIV + lane] = centroid_row(A.conf_in + 3 * (size_t)a0, N, lane);
       __syncwarp();
     } else {
-      compute_pivot(vb, torsh, S, s_hl, n, N, hx, hv, true, lane);
+      compute_pivot(vb, S, N, hx, true, lane);
     }
 
     PH(0)
@@ -801,6 +793,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
               x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
             st3(torsh + 3 * h, x);
+            st3(hx + 3 * s_hl[h], x);
           }
           hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
           prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane);
@@ -810,7 +803,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         if (lane == 0) S[S_GEO] = bv;
         __syncwarp();
         // new pivot = centroid of the adopted conformation (vb is free here)
-        compute_pivot(vb, torsh, S, s_hl, n, N, hx, hv, true, lane);
+        compute_pivot(vb, S, N, hx, true, lane);
         PH(bj < 12 ? 5 : 6)
       } else {
         if (lane == 0) {
@@ -838,7 +831,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
       #pragma unroll 1
       for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
     } else {
-      full_conformation(A.o.conf + ck, torsh, S, s_hl, n, N, hx, hv, true, lane);
+      full_conformation(A.o.conf + ck, S, N, hx, true, lane);
     }
     const size_t tk = (size_t)t0 * k + (size_t)r * m;
     #pragma unroll 1
