@@ -157,7 +157,8 @@ struct search_args {
   int *work;
   int n_lig;             // ligands of this launch (each: k restarts)
   const int *lig_index;  // bucket launches: launch ligand -> batch ligand (NULL: identity)
-  double *hscr;          // per resident warp: 3 * Nmax doubles (hydrogens' torsioned frame)
+  double *hscr;          // global scratch: per resident warp 3 * (Nmax + nmax * mmax), then per CTA 14 * mmax
+  int scr_warps;         // warp slots in the scratch
   int Nmax, nmax, mmax, dmax;
   int warp_doubles;
   int cta_doubles;       // CTA-shared ligand staging (after the palette)
@@ -341,6 +342,10 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   // the stage-t prefix positions of the torsion items (3 * nmax * mmax)
   double *hx = A.hscr + (size_t)(blockIdx.x * kWarps + warp) * 3 * (A.Nmax + A.nmax * A.mmax);
   double *pc = hx + 3 * A.Nmax;
+  // per-CTA global slot (dock path): the start matrices of flatten's angles
+  // and their sin/cos, computed once per ligand for all its restarts
+  double *M0 = A.hscr + (size_t)A.scr_warps * 3 * (A.Nmax + A.nmax * A.mmax) + (size_t)blockIdx.x * 14 * A.mmax;
+  double *sc0 = M0 + 12 * A.mmax;
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
   double *Rj = W + A.o_Rj;       // 6 spin neighbours x kRow: R at 0, t at 10, q at 14 (16-byte aligned)
@@ -360,6 +365,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   const grid_view &g = A.p.g;
   const packed_grid &pg = A.pg;
   const bool ls_mode = A.pose_in != nullptr;
+  const bool dock_path = !ls_mode && A.ang_in == nullptr;  // start angles = flatten's lattice angles
   const int k = ls_mode ? 1 : A.c.k;
   const int nmax = A.nmax;
   PH_DECL
@@ -414,8 +420,21 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         #pragma unroll 1
         for (int i = 0; i < cnt; ++i) s_tit[off + i] = titems[2 * off + i];
       }
+      if (dock_path) {
+        #pragma unroll 1
+        for (int u = threadIdx.x; u < m; u += blockDim.x) {
+          const int li = A.f.idx[t0 + u];
+          sc0[2 * u] = c_lattice_sc_dev(2 * li);
+          sc0[2 * u + 1] = c_lattice_sc_dev(2 * li + 1);
+        }
+      }
     }
     __syncthreads();
+    if (dock_path) {
+      // flatten already rejected ligands whose axes degenerate at these angles
+      if (threadIdx.x == 0 && m > 0) chain_mats(0, sc0[0], sc0[1], m, s_ep, s_epm, M0, sc0, M0);
+      __syncthreads();
+    }
     const int J = 12 + 2 * m;
 
   while (true) {  // restarts of this ligand, one per warp at a time
@@ -448,24 +467,36 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
     }
     if (lane == 0) S[S_ERR] = 0.0;
     __syncwarp();
-    if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, s_ep, s_epm, Mcur, sccur, Mcur))
-      S[S_ERR] = 1.0;
-    __syncwarp();
-    if (S[S_ERR] != 0.0) {
-      if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
-      continue;
-    }
-    // torsioned frame (search.cpp:115), heavy atoms
-    #pragma unroll 1
-    for (int h = lane; h < n; h += 32) {
-      d3 x = ld3(s_bh + 3 * h);
+    if (dock_path) {
+      // start matrices from the CTA slot; the torsioned frame is flatten's
+      // conformation (the same per-atom operations, bit for bit)
       #pragma unroll 1
-      for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
-        x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
-      st3(torsh + 3 * h, x);
-      st3(hx + 3 * s_hl[h], x);  // every atom's frame also in hx (pivots, outputs)
+      for (int i = lane; i < 12 * m; i += 32) Mcur[i] = M0[i];
+      #pragma unroll 1
+      for (int i = lane; i < 3 * N; i += 32) hx[i] = A.f.xyz[3 * (size_t)a0 + i];
+      #pragma unroll 1
+      for (int h = lane; h < n; h += 32) st3(torsh + 3 * h, ld3(A.f.xyz + 3 * ((size_t)a0 + s_hl[h])));
+    } else {
+      if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, s_ep, s_epm, Mcur, sccur, Mcur))
+        S[S_ERR] = 1.0;
+      __syncwarp();
+      if (S[S_ERR] != 0.0) {
+        if (lane == 0) A.o.status[item] = VS_LIG_DEGENERATE_AXIS;
+        continue;
+      }
+      // torsioned frame (search.cpp:115)
+      #pragma unroll 1
+      for (int h = lane; h < n; h += 32) {
+        d3 x = ld3(s_bh + 3 * h);
+        #pragma unroll 1
+        for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
+          x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
+        st3(torsh + 3 * h, x);
+        st3(hx + 3 * s_hl[h], x);  // every atom's frame also in hx (pivots, outputs)
+      }
+      hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
     }
-    hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
+    __syncwarp();
     prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane);
     __syncwarp();
     // initial_poses entry point: the flat centroid of these angles
@@ -954,7 +985,7 @@ extern "C" int vs_debug_phase_read(unsigned long long *out, int reset) {
 // torsion items' prefix positions.
 size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms) {
   const size_t N = nmax_atoms > 0 ? nmax_atoms : 1, n = nmax_heavy > 0 ? nmax_heavy : 1, m = mmax > 0 ? mmax : 1;
-  return (size_t)num_sms * 16 * 3 * (N + n * m) * sizeof(double);
+  return ((size_t)num_sms * 16 * 3 * (N + n * m) + (size_t)num_sms * 16 * 14 * m) * sizeof(double);
 }
 
 int search_warps_per_cta() { return kWarps; }
@@ -970,6 +1001,7 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
                           int n_lig, int dmax) {
   search_args A{};
   A.hscr = static_cast<double *>(args_buf);
+  A.scr_warps = num_sms * 16;
   A.b = b;
   A.p = p;
   A.pg = p.packed;
@@ -992,6 +1024,7 @@ cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const 
                                  int num_sms, cudaStream_t s, void *args_buf) {
   search_args A{};
   A.hscr = static_cast<double *>(args_buf);
+  A.scr_warps = num_sms * 16;
   A.b = b;
   A.p = p;
   A.pg = p.packed;
@@ -1015,6 +1048,7 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
                                 void *args_buf) {
   search_args A{};
   A.hscr = static_cast<double *>(args_buf);
+  A.scr_warps = num_sms * 16;
   A.b = b;
   A.p = p;
   A.pg = p.packed;
