@@ -258,10 +258,10 @@ __device__ __noinline__ int chain_warp(int vbase, int ufrom, int m, const double
 // The search keeps only heavy atoms in shared memory: hydrogens matter only
 // for pivots and outputs.
 __device__ __noinline__ void hydrogen_frame(double *hx, int N, const double *base, const uint32_t *tm,
-                                            const uint8_t *heavy, const double *Mcur, int lane) {
+                                            const uint8_t *heavy, const double *Mcur, uint32_t moved, int lane) {
   #pragma unroll 1
   for (int a = lane; a < N; a += 32) {
-    if (heavy[a]) continue;
+    if (heavy[a] || (moved != 0xffffffffu && !(tm[a] & moved))) continue;  // all ones: every hydrogen
     d3 x = ld3(base + 3 * a);
     #pragma unroll 1
     for (uint32_t bb = tm[a]; bb; bb &= bb - 1u) x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         st3(torsh + 3 * h, x);
         st3(hx + 3 * s_hl[h], x);  // every atom's frame also in hx (pivots, outputs)
       }
-      hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
+      hydrogen_frame(hx, N, base, tm, hv, Mcur, 0xffffffffu, lane);
     }
     __syncwarp();
     prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane);
@@ -817,16 +817,26 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           mvar_valid = false;
           chain_from = t;
           __syncwarp();
+          // only atoms whose coordinates depend on torsion t move: heavy
+          // atoms of D_t continue from their cached stage-t prefixes through
+          // the new matrices u >= t; hydrogens moved by t or by a torsion
+          // whose axis depends on t are re-torsioned from base
+          uint32_t dep = 1u << t;
           #pragma unroll 1
-          for (int h = lane; h < n; h += 32) {
-            d3 x = ld3(s_bh + 3 * h);
+          for (int u = t + 1; u < m; ++u)
+            if ((s_epm[2 * u] | s_epm[2 * u + 1]) & dep) dep |= 1u << u;
+          #pragma unroll 1
+          for (int i = lane; i < s_dcnt[t]; i += 32) {
+            const int p = s_doff[t] + i;
+            const int h = s_tit[p] & 255;
+            d3 x = ld3(pc + 3 * p);
             #pragma unroll 1
-            for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
+            for (uint32_t bb = (s_tmh[h] & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u)
               x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
             st3(torsh + 3 * h, x);
             st3(hx + 3 * s_hl[h], x);
           }
-          hydrogen_frame(hx, N, base, tm, hv, Mcur, lane);
+          hydrogen_frame(hx, N, base, tm, hv, Mcur, dep, lane);
           prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane);
         }
         #pragma unroll 1
