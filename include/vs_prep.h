@@ -37,6 +37,9 @@ vs_status vs_prep_smiles_batch(int32_t n, const char *const *smiles, int32_t mod
 /* Borrowed SoA view of the set (valid until vs_ligand_set_free). */
 vs_status vs_ligand_set_view(const vs_ligand_set *set, vs_ligand_batch *view, const int32_t **status);
 const char *vs_ligand_set_error(const vs_ligand_set *set, int32_t i);
+/* Name of entry i (the SMILES for prepared sets, the record name for
+ * decoded ones: the string the reference writes as the output row key). */
+const char *vs_ligand_set_name(const vs_ligand_set *set, int32_t i);
 void vs_ligand_set_free(vs_ligand_set *set);
 
 /* Graph analysis of ligand i of a batch (host): detect_torsions

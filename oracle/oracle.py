@@ -288,6 +288,21 @@ class Oracle:
         finally:
             self._free(h)
 
+    def encode_prepared(self, smiles: str, mode: int = 0, quantize: bool = True) -> bytes:
+        """encode_record (binary_codec.cpp:129-163) of the reference's own
+        prepared ligand (see prepare)."""
+        assert self.kind == "ref"
+        h = self._prep(smiles.encode(), mode, 1 if quantize else 0)
+        if not h:
+            raise ValueError(self._err().decode())
+        try:
+            n = self._encode(h, None, 0)
+            buf = np.zeros(n, dtype=np.uint8)
+            self._encode(h, abi.ptr(buf, C.c_uint8), n)
+            return buf.tobytes()
+        finally:
+            self._free(h)
+
     def decode_record(self, data: bytes, offset: int):
         buf = np.frombuffer(data, dtype=np.uint8).copy()
         nxt = C.c_int64(0)

@@ -149,42 +149,105 @@ def prepare_smiles(smiles: Sequence[str], mode: int = 1, nthreads: int = 8, stri
     h = C.c_void_p()
     native.check(L.vs_prep_smiles_batch(len(enc), arr, mode, nthreads, C.byref(h)), "vs_prep_smiles_batch")
     try:
-        v = abi.LigandBatchDesc()
-        st = C.POINTER(C.c_int32)()
-        L.vs_ligand_set_view(h, C.byref(v), C.byref(st))
-        n = len(enc)
-        out = []
-        ao = np.ctypeslib.as_array(v.atom_offset, (n + 1,)).copy()
-        bo = np.ctypeslib.as_array(v.bond_offset, (n + 1,)).copy()
-        to = np.ctypeslib.as_array(v.torsion_offset, (n + 1,)).copy()
-        na, nb, nt = int(ao[-1]), int(bo[-1]), int(to[-1])
+        ligs, status, errors = _ligands_of_set(h, len(enc), list(smiles))
+    finally:
+        L.vs_ligand_set_free(h)
+    if strict:
+        for i, st in enumerate(status):
+            if st != 0:
+                raise ValueError(errors[i])
+    return ligs
 
-        def arr_of(p, shape, dt):
-            if int(np.prod(shape)) == 0:
-                return np.zeros(shape, dtype=dt)
-            return np.ctypeslib.as_array(p, shape).astype(dt, copy=True)
 
-        xyz = arr_of(v.xyz, (na * 3,), np.float64).reshape(-1, 3)
-        el = arr_of(v.element, (na,), np.uint8)
-        hv = arr_of(v.is_heavy, (na,), np.uint8)
-        ba = arr_of(v.bond_a, (nb,), np.uint16)
-        bb = arr_of(v.bond_b, (nb,), np.uint16)
-        bord = arr_of(v.bond_order, (nb,), np.uint8)
-        tb = arr_of(v.torsion_bond, (nt,), np.uint16)
-        ro = np.ctypeslib.as_array(v.right_offset, (nt + 1,)).copy()
-        ra = arr_of(v.right_atoms, (int(ro[-1]),), np.uint16)
-        status = np.ctypeslib.as_array(st, (n,)).copy() if n else np.zeros(0, np.int32)
-        for i in range(n):
-            if status[i] != 0:
-                if strict:
-                    raise ValueError(L.vs_ligand_set_error(h, i).decode())
-                out.append(None)
-                continue
-            a0, a1, b0, b1, t0, t1 = ao[i], ao[i + 1], bo[i], bo[i + 1], to[i], to[i + 1]
-            out.append(Ligand(smiles[i], xyz[a0:a1].copy(), el[a0:a1].copy(), hv[a0:a1].copy(),
-                              np.stack([ba[b0:b1], bb[b0:b1]], axis=1).copy(), bord[b0:b1].copy(),
-                              tb[t0:t1].copy(), [ra[ro[t]:ro[t + 1]].copy() for t in range(t0, t1)]))
-        return out
+def _ligands_of_set(h, n: int, names=None):
+    """Ligand objects of a vs_ligand_set (None for failed entries), with the
+    per-entry status and error text."""
+    L = native.lib()
+    v = abi.LigandBatchDesc()
+    st = C.POINTER(C.c_int32)()
+    L.vs_ligand_set_view(h, C.byref(v), C.byref(st))
+    out = []
+    ao = np.ctypeslib.as_array(v.atom_offset, (n + 1,)).copy()
+    bo = np.ctypeslib.as_array(v.bond_offset, (n + 1,)).copy()
+    to = np.ctypeslib.as_array(v.torsion_offset, (n + 1,)).copy()
+    na, nb, nt = int(ao[-1]), int(bo[-1]), int(to[-1])
+
+    def arr_of(p, shape, dt):
+        if int(np.prod(shape)) == 0:
+            return np.zeros(shape, dtype=dt)
+        return np.ctypeslib.as_array(p, shape).astype(dt, copy=True)
+
+    xyz = arr_of(v.xyz, (na * 3,), np.float64).reshape(-1, 3)
+    el = arr_of(v.element, (na,), np.uint8)
+    hv = arr_of(v.is_heavy, (na,), np.uint8)
+    ba = arr_of(v.bond_a, (nb,), np.uint16)
+    bb = arr_of(v.bond_b, (nb,), np.uint16)
+    bord = arr_of(v.bond_order, (nb,), np.uint8)
+    tb = arr_of(v.torsion_bond, (nt,), np.uint16)
+    ro = np.ctypeslib.as_array(v.right_offset, (nt + 1,)).copy()
+    ra = arr_of(v.right_atoms, (int(ro[-1]),), np.uint16)
+    status = np.ctypeslib.as_array(st, (n,)).copy() if n else np.zeros(0, np.int32)
+    errors = [L.vs_ligand_set_error(h, i).decode() for i in range(n)]
+    for i in range(n):
+        if status[i] != 0:
+            out.append(None)
+            continue
+        name = names[i] if names is not None else L.vs_ligand_set_name(h, i).decode(errors="replace")
+        a0, a1, b0, b1, t0, t1 = ao[i], ao[i + 1], bo[i], bo[i + 1], to[i], to[i + 1]
+        out.append(Ligand(name, xyz[a0:a1].copy(), el[a0:a1].copy(), hv[a0:a1].copy(),
+                          np.stack([ba[b0:b1], bb[b0:b1]], axis=1).copy(), bord[b0:b1].copy(),
+                          tb[t0:t1].copy(), [ra[ro[t]:ro[t + 1]].copy() for t in range(t0, t1)]))
+    return out, status, errors
+
+
+# ---------------------------------------------------------------- records
+XSLB_HEADER = b"XSLB\x01\x00\x00\x00"  # xslb_header (binary_codec.cpp:115-118)
+
+
+def encode_records(ligands, names=None) -> bytes:
+    """encode_record (binary_codec.cpp:129-163) of every ligand, back to back
+    (no file header); names default to the ligands' names."""
+    b = _batch(ligands)
+    nm = names if names is not None else [getattr(l, "name", "") or "" for l in b.ligands]
+    enc = [str(x).encode() for x in nm]
+    arr = (C.c_char_p * max(len(enc), 1))(*enc)
+    L = native.lib()
+    need = -L.vs_encode_records(C.byref(b.desc()), arr, None, 0)
+    buf = (C.c_uint8 * max(need, 1))()
+    used = L.vs_encode_records(C.byref(b.desc()), arr, buf, need)
+    if used < 0:
+        raise RuntimeError("vs_encode_records: buffer too small")
+    return bytes(buf[:used])
+
+
+def frame_records(data: bytes, start: int = 0, max_records: int | None = None) -> np.ndarray:
+    """Record start offsets from `start` along the length chain."""
+    L = native.lib()
+    buf = np.frombuffer(data, dtype=np.uint8)
+    cap = max_records if max_records is not None else max(1, len(data) // 8)
+    offs = np.zeros(cap, dtype=np.int64)
+    nxt = C.c_int64(0)
+    n = L.vs_xslb_frame(abi.ptr(buf, C.c_uint8), len(data), start, cap, abi.ptr(offs, C.c_int64), C.byref(nxt))
+    if n < 0:
+        raise ValueError("bad framing arguments")
+    return offs[:n]
+
+
+def decode_records(data: bytes, offsets=None, ctx: Context | None = None):
+    """GPU decode_record (binary_codec.cpp:165-222) of the records at
+    `offsets` (default: framed from 0): (ligands, status, errors); a ligand
+    is None where the record fails with the reference's CodecError."""
+    ctx = ctx or default_context()
+    if offsets is None:
+        offsets = frame_records(data)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    buf = np.frombuffer(data, dtype=np.uint8)
+    h = C.c_void_p()
+    L = native.lib()
+    native.check(L.vs_decode_records(ctx.handle, abi.ptr(buf, C.c_uint8), len(data), abi.ptr(offs, C.c_int64),
+                                     len(offs), C.byref(h)), "vs_decode_records")
+    try:
+        return _ligands_of_set(h, len(offs))
     finally:
         L.vs_ligand_set_free(h)
 

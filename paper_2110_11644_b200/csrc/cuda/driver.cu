@@ -18,7 +18,9 @@
 #include <vector>
 
 #include "../../../include/vs_crtrig.h"
+#include "../../../include/vs_codec.h"
 #include "../../../include/vs_dock.h"
+#include "../host/ligand_set.hpp"
 #include "kernels.cuh"
 
 namespace {
@@ -82,6 +84,9 @@ struct vs_context {
       out_iters, out_adopts, work;
   DevBuf results, best_ang, best_conf, counters, spin, fibq, stepsc, flat_index;
   DevBuf aux0, aux1, aux2, aux3, search_args, lig_index;
+  // record decode
+  DevBuf dec_bytes, dec_offs, dec_aoff, dec_boff, dec_toff, dec_rsoff, dec_xyz, dec_elem, dec_heavy, dec_order,
+      dec_ba, dec_bb, dec_tbond, dec_rslots, dec_rcount, dec_status;
 };
 
 struct vs_pocket {
@@ -1105,3 +1110,159 @@ vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ codec
+namespace {
+
+const char *record_error(int st) {
+  switch (st) {
+    case VS_REC_BAD_MARKER: return "bad sync marker";
+    case VS_REC_TRUNCATED: return "truncated record";
+    case VS_REC_LENGTH_MISMATCH: return "record length mismatch";
+    case VS_REC_BAD_ELEMENT: return "invalid element code";
+    case VS_REC_NONFINITE: return "non-finite coordinate";
+    case VS_REC_BAD_BOND: return "invalid bond";
+    case VS_REC_BAD_BOND_ORDER: return "invalid bond order";
+    case VS_REC_BAD_TORSION_INDEX: return "invalid torsion bond index";
+    case VS_REC_NOT_BRIDGE: return "invalid torsion: torsion bond is not a bridge";
+    case VS_REC_DISCONNECTED: return "record graph is disconnected";
+    case VS_REC_TOO_LARGE: return "record too large for the GPU decoder (> 4096 atoms)";
+    default: return "";
+  }
+}
+
+uint32_t rd16h(const uint8_t *p) { return (uint32_t)p[0] | ((uint32_t)p[1] << 8); }
+
+}  // namespace
+
+// decode_record (binary_codec.cpp:165-222) of n records on the GPU: the host
+// reads only the framing (marker, length, name, counts) to size the outputs;
+// payloads, validation and torsion partitions run in k_decode (codec.cu).
+extern "C" vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, int64_t size, const int64_t *offsets,
+                                       int32_t n, vs_ligand_set **out) {
+  if (!ctx || !out || n < 0 || (n > 0 && (!bytes || !offsets))) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  auto *set = new vs_ligand_set;
+  const size_t N = static_cast<size_t>(n);
+  std::vector<int32_t> st(N, VS_REC_OK), na(N, 0), nb(N, 0), nt(N, 0);
+  set->names.assign(N, std::string());
+  for (size_t r = 0; r < N; ++r) {
+    const int64_t at = offsets[r];
+    if (at < 0 || at + 2 > size || bytes[at] != 0xD0 || bytes[at + 1] != 0xC5) {
+      st[r] = VS_REC_BAD_MARKER;
+      continue;
+    }
+    if (at + 6 > size) {
+      st[r] = VS_REC_TRUNCATED;
+      continue;
+    }
+    const uint64_t len = rd16h(bytes + at + 2) | (static_cast<uint64_t>(rd16h(bytes + at + 4)) << 16);
+    const int64_t end = at + 6 + static_cast<int64_t>(len);
+    if (end > size || at + 8 > size) {
+      st[r] = VS_REC_TRUNCATED;
+      continue;
+    }
+    const uint32_t name_len = rd16h(bytes + at + 6);
+    if (at + 8 + static_cast<int64_t>(name_len) + 6 > size) {
+      st[r] = VS_REC_TRUNCATED;
+      continue;
+    }
+    const uint8_t *q = bytes + at + 8 + name_len;
+    const uint32_t a = rd16h(q), b = rd16h(q + 2), t = rd16h(q + 4);
+    const uint64_t payload = 2ull + name_len + 6 + 14ull * a + 5ull * b + 2ull * t;
+    if (payload != len) {
+      st[r] = VS_REC_LENGTH_MISMATCH;
+      continue;
+    }
+    set->names[r].assign(reinterpret_cast<const char *>(bytes + at + 8), name_len);
+    na[r] = static_cast<int32_t>(a);
+    nb[r] = static_cast<int32_t>(b);
+    nt[r] = static_cast<int32_t>(t);
+  }
+  std::vector<int32_t> aoff(N + 1, 0), boff(N + 1, 0), toff(N + 1, 0);
+  for (size_t r = 0; r < N; ++r) {
+    aoff[r + 1] = aoff[r] + na[r];
+    boff[r + 1] = boff[r] + nb[r];
+    toff[r + 1] = toff[r] + nt[r];
+  }
+  std::vector<int64_t> rsoff(static_cast<size_t>(toff[N]) + 1, 0);
+  for (size_t r = 0; r < N; ++r)
+    for (int k = 0; k < nt[r]; ++k) rsoff[toff[r] + k + 1] = rsoff[toff[r] + k] + na[r];
+  const size_t atoms = aoff[N], bonds = boff[N], tors = toff[N], slots = rsoff.back();
+  vs_status rc;
+  cudaStream_t s = ctx->stream;
+  if ((rc = h2d(ctx->dec_bytes, bytes, static_cast<size_t>(std::max<int64_t>(size, 0)), s))) return rc;
+  if ((rc = h2d(ctx->dec_offs, offsets, N, s))) return rc;
+  if ((rc = h2d(ctx->dec_aoff, aoff.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->dec_boff, boff.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->dec_toff, toff.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->dec_rsoff, rsoff.data(), rsoff.size(), s))) return rc;
+  if ((rc = h2d(ctx->dec_status, st.data(), N, s))) return rc;
+  CUDA_TRY(ctx->dec_xyz.ensure(sizeof(double) * 3 * std::max<size_t>(atoms, 1)));
+  CUDA_TRY(ctx->dec_elem.ensure(std::max<size_t>(atoms, 1)));
+  CUDA_TRY(ctx->dec_heavy.ensure(std::max<size_t>(atoms, 1)));
+  CUDA_TRY(ctx->dec_order.ensure(std::max<size_t>(bonds, 1)));
+  CUDA_TRY(ctx->dec_ba.ensure(sizeof(uint16_t) * std::max<size_t>(bonds, 1)));
+  CUDA_TRY(ctx->dec_bb.ensure(sizeof(uint16_t) * std::max<size_t>(bonds, 1)));
+  CUDA_TRY(ctx->dec_tbond.ensure(sizeof(uint16_t) * std::max<size_t>(tors, 1)));
+  CUDA_TRY(ctx->dec_rslots.ensure(sizeof(uint16_t) * std::max<size_t>(slots, 1)));
+  CUDA_TRY(ctx->dec_rcount.ensure(sizeof(int) * std::max<size_t>(tors, 1)));
+  CUDA_TRY(vsd::launch_decode(ctx->dec_bytes.as<uint8_t>(), ctx->dec_offs.as<int64_t>(), n, ctx->dec_aoff.as<int>(),
+                              ctx->dec_boff.as<int>(), ctx->dec_toff.as<int>(), ctx->dec_rsoff.as<int64_t>(),
+                              ctx->dec_xyz.as<double>(), ctx->dec_elem.as<uint8_t>(), ctx->dec_heavy.as<uint8_t>(),
+                              ctx->dec_order.as<uint8_t>(), ctx->dec_ba.as<uint16_t>(), ctx->dec_bb.as<uint16_t>(),
+                              ctx->dec_tbond.as<uint16_t>(), ctx->dec_rslots.as<uint16_t>(), ctx->dec_rcount.as<int>(),
+                              ctx->dec_status.as<int>(), s));
+  std::vector<double> xyz(3 * atoms);
+  std::vector<uint8_t> elem(atoms), heavy(atoms), order(bonds);
+  std::vector<uint16_t> ba(bonds), bb(bonds), tb(tors), rsl(slots);
+  std::vector<int> rcount(tors);
+  auto d2h = [&](void *dst, const DevBuf &src, size_t bytes_) -> cudaError_t {
+    return bytes_ ? cudaMemcpyAsync(dst, src.p, bytes_, cudaMemcpyDeviceToHost, s) : cudaSuccess;
+  };
+  CUDA_TRY(d2h(xyz.data(), ctx->dec_xyz, sizeof(double) * 3 * atoms));
+  CUDA_TRY(d2h(elem.data(), ctx->dec_elem, atoms));
+  CUDA_TRY(d2h(heavy.data(), ctx->dec_heavy, atoms));
+  CUDA_TRY(d2h(order.data(), ctx->dec_order, bonds));
+  CUDA_TRY(d2h(ba.data(), ctx->dec_ba, sizeof(uint16_t) * bonds));
+  CUDA_TRY(d2h(bb.data(), ctx->dec_bb, sizeof(uint16_t) * bonds));
+  CUDA_TRY(d2h(tb.data(), ctx->dec_tbond, sizeof(uint16_t) * tors));
+  CUDA_TRY(d2h(rsl.data(), ctx->dec_rslots, sizeof(uint16_t) * slots));
+  CUDA_TRY(d2h(rcount.data(), ctx->dec_rcount, sizeof(int) * tors));
+  CUDA_TRY(d2h(st.data(), ctx->dec_status, sizeof(int32_t) * N));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // the set: failed records become empty entries with the reference's message
+  set->status.assign(N, 0);
+  set->errors.assign(N, std::string());
+  set->atom_off.push_back(0);
+  set->bond_off.push_back(0);
+  set->tors_off.push_back(0);
+  set->right_off.push_back(0);
+  for (size_t r = 0; r < N; ++r) {
+    set->status[r] = st[r];
+    if (st[r] == VS_REC_OK) {
+      for (int a = aoff[r]; a < aoff[r + 1]; ++a) {
+        for (int c = 0; c < 3; ++c) set->xyz.push_back(xyz[3 * static_cast<size_t>(a) + c]);
+        set->elem.push_back(elem[a]);
+        set->heavy.push_back(heavy[a]);
+      }
+      for (int k = boff[r]; k < boff[r + 1]; ++k) {
+        set->ba.push_back(ba[k]);
+        set->bb.push_back(bb[k]);
+        set->border.push_back(order[k]);
+      }
+      for (int k = toff[r]; k < toff[r + 1]; ++k) {
+        set->tbond.push_back(tb[k]);
+        set->ratoms.insert(set->ratoms.end(), rsl.begin() + rsoff[k], rsl.begin() + rsoff[k] + rcount[k]);
+        set->right_off.push_back(static_cast<int32_t>(set->ratoms.size()));
+      }
+    } else {
+      set->errors[r] = record_error(st[r]);
+    }
+    set->atom_off.push_back(static_cast<int32_t>(set->elem.size()));
+    set->bond_off.push_back(static_cast<int32_t>(set->ba.size()));
+    set->tors_off.push_back(static_cast<int32_t>(set->tbond.size()));
+  }
+  *out = set;
+  return VS_OK;
+}

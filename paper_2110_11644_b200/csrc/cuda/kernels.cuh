@@ -116,6 +116,10 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
                           int num_sms, cudaStream_t s, int *launches, void *args_buf,
                           const int *lig_index = nullptr, int n_lig = 0, int dmax = 0);
 // device buffer size the search launchers need for their argument block
+cudaError_t launch_decode(const uint8_t *bytes, const int64_t *offs, int n, const int *atom_off, const int *bond_off,
+                          const int *tors_off, const int64_t *rs_off, double *xyz, uint8_t *elem, uint8_t *heavy,
+                          uint8_t *border, uint16_t *ba, uint16_t *bb, uint16_t *tbond, uint16_t *rslots, int *rcount,
+                          int *status, cudaStream_t s);
 size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms);
 // dynamic shared memory of one k_search CTA for the given ligand maxima
 size_t search_smem_bytes(int N, int n, int m, int dtot);

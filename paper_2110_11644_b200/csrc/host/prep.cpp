@@ -658,14 +658,7 @@ bool counts(const std::string &smiles, int *heavy, int *rot) {
 }  // namespace vsprep_internal
 
 // =================================================================== C API
-struct vs_ligand_set {
-  std::vector<int32_t> status;
-  std::vector<std::string> errors;
-  std::vector<int32_t> atom_off, bond_off, tors_off, right_off;
-  std::vector<double> xyz;
-  std::vector<uint8_t> elem, heavy, border;
-  std::vector<uint16_t> ba, bb, tbond, ratoms;
-};
+#include "ligand_set.hpp"
 
 extern "C" {
 
@@ -676,6 +669,8 @@ vs_status vs_prep_smiles_batch(int32_t n, const char *const *smiles, int32_t mod
   auto *set = new vs_ligand_set;
   set->status.assign(static_cast<std::size_t>(n), 0);
   set->errors.assign(static_cast<std::size_t>(n), std::string());
+  set->names.resize(static_cast<std::size_t>(n));
+  for (int32_t i = 0; i < n; ++i) set->names[static_cast<std::size_t>(i)] = smiles[i] ? smiles[i] : "";
   std::atomic<int> next{0};
   auto work = [&] {
     for (int i = next++; i < n; i = next++) {
@@ -744,6 +739,11 @@ vs_status vs_ligand_set_view(const vs_ligand_set *s, vs_ligand_batch *v, const i
 const char *vs_ligand_set_error(const vs_ligand_set *s, int32_t i) {
   if (!s || i < 0 || static_cast<std::size_t>(i) >= s->errors.size()) return "";
   return s->errors[static_cast<std::size_t>(i)].c_str();
+}
+
+const char *vs_ligand_set_name(const vs_ligand_set *s, int32_t i) {
+  if (!s || i < 0 || static_cast<std::size_t>(i) >= s->names.size()) return "";
+  return s->names[static_cast<std::size_t>(i)].c_str();
 }
 
 void vs_ligand_set_free(vs_ligand_set *s) { delete s; }
