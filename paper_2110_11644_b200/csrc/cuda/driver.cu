@@ -1232,6 +1232,29 @@ extern "C" vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, in
   CUDA_TRY(d2h(st.data(), ctx->dec_status, sizeof(int32_t) * N));
   CUDA_TRY(cudaStreamSynchronize(s));
   // the set: failed records become empty entries with the reference's message
+  bool all_ok = true;
+  for (size_t r = 0; r < N && all_ok; ++r) all_ok = st[r] == VS_REC_OK;
+  if (all_ok) {  // the device arrays already are the set's layout
+    set->status.assign(N, 0);
+    set->errors.assign(N, std::string());
+    set->atom_off = std::move(aoff);
+    set->bond_off = std::move(boff);
+    set->tors_off = std::move(toff);
+    set->xyz = std::move(xyz);
+    set->elem = std::move(elem);
+    set->heavy = std::move(heavy);
+    set->border = std::move(order);
+    set->ba = std::move(ba);
+    set->bb = std::move(bb);
+    set->tbond = std::move(tb);
+    set->right_off.assign(tors + 1, 0);
+    for (size_t k = 0; k < tors; ++k) set->right_off[k + 1] = set->right_off[k] + rcount[k];
+    set->ratoms.resize(static_cast<size_t>(set->right_off[tors]));
+    for (size_t k = 0; k < tors; ++k)
+      std::memcpy(set->ratoms.data() + set->right_off[k], rsl.data() + rsoff[k], sizeof(uint16_t) * rcount[k]);
+    *out = set;
+    return VS_OK;
+  }
   set->status.assign(N, 0);
   set->errors.assign(N, std::string());
   set->atom_off.push_back(0);
