@@ -954,6 +954,8 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
+  // the global scratch holds 16 warps per SM (search_scratch_bytes)
+  if (per_sm > 16 / kWarps) per_sm = 16 / kWarps;
 #ifdef VS_PROF_CTAS_PER_SM
   per_sm = VS_PROF_CTAS_PER_SM;  // development: phase timing without co-resident warps
 #endif
