@@ -43,6 +43,18 @@ constexpr int kWarps = VS_SEARCH_WARPS;
 #ifndef VS_SEARCH_GROUP
 #define VS_SEARCH_GROUP 12
 #endif
+// Development bounds checks (build with -DVS_DEBUG_CHECKS): trap on an
+// out-of-range shared-memory / scratch index instead of corrupting state.
+#ifdef VS_DEBUG_CHECKS
+#define VS_CHECK(c) \
+  do {              \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define VS_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 constexpr int kPalDoubles = 32;  // palette / code-pair table at the start of shared memory
 constexpr int kRow = 18;  // spin-neighbour row: R (9), pad, t (3), pad, q (4)
 constexpr int kGroup = VS_SEARCH_GROUP;  // neighbours per group (>= 12, even; 12 measured best)
@@ -346,6 +358,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
   // and their sin/cos, computed once per ligand for all its restarts
   double *M0 = A.hscr + (size_t)A.scr_warps * 3 * (A.Nmax + A.nmax * A.mmax) + (size_t)blockIdx.x * 14 * A.mmax;
   double *sc0 = M0 + 12 * A.mmax;
+  VS_CHECK((int)(blockIdx.x * kWarps + warp) < A.scr_warps);
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
   double *Rj = W + A.o_Rj;       // 6 spin neighbours x kRow: R at 0, t at 10, q at 14 (16-byte aligned)
@@ -728,6 +741,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
                 ++rj;
               }
             } else {
+              VS_CHECK(s_doff[tlo] + (it >> 1) < A.dmax);
               const uint32_t e = ti[it >> 1];
               const int v = ((e >> 8) & 63) | (it & 1), t = v >> 1;
               h = e & 255;
@@ -735,6 +749,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
               const uint32_t mask = s_tmh[h];
               col = (int)(mask >> 31);
               const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;  // matrix u >= t at Mv + 12u
+              VS_CHECK(t < m && mvar_off(v, m - 1, m) + 12 <= 12 * A.mmax * (A.mmax + 1) && h < n);
               #pragma unroll 1
               for (uint32_t bb = (mask & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u)
                 x = torsion_apply_a(Mv + 12 * (__ffs(bb) - 1), x);
@@ -743,6 +758,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
               T = S + S_T;
             }
             bool out;
+            VS_CHECK(row >= 0 && row < kGroup && h >= 0 && h < nmax);
             vb[row * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, col), out);
           }
         }
