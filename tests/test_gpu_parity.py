@@ -213,6 +213,28 @@ def test_dock_bit_exact_vs_oracle(env, k, rescored):
     assert np.array_equal(got.counters, want["counters"])  # Appendix B work counters, integer-exact
 
 
+@pytest.mark.parametrize("kw", [
+    dict(restarts=6, rescored=6, max_iterations=3),                        # iteration cap
+    dict(restarts=6, rescored=4, min_translation=0.001),                    # 10 step levels
+    dict(restarts=6, rescored=6, step_torsion=1.0, step_rotation=0.8, step_translation=2.0),  # coarse, arbitrary angles
+    dict(restarts=10, rescored=10, rmsd_threshold=0.5),                      # many leaders
+    dict(restarts=10, rescored=3, rmsd_threshold=10.0),                      # one leader
+    dict(restarts=4, rescored=4, flatten_max_sweeps=1),
+    dict(restarts=40, rescored=7),                                           # k > 32: CTA select
+])
+def test_dock_bit_exact_config_variations(env, kw):
+    ctx, pocket, host, b = env
+    sub = LigandBatch(b.ligands[:24])
+    cfg = abi.ScoringConfig(**kw)
+    got = api.dock_and_score_batch(pocket, sub, cfg, ctx, want_counters=True)
+    want = Oracle("port", trig=1).dock_batch(host, sub, cfg, nthreads=THREADS, want_counters=True)
+    for f in ("status", "best_score", "best_geo_score", "rotation", "translation", "scoring_evals", "clash_pairs",
+              "oob_samples", "n_survivors"):
+        assert np.array_equal(got.results[f], want["results"][f]), (kw, f)
+    assert np.array_equal(got.best_conformation, want["conformation"]), kw
+    assert np.array_equal(got.counters, want["counters"]), kw
+
+
 def test_dock_default_config_256_restarts(env):
     ctx, pocket, host, b = env
     sub = LigandBatch(b.ligands[:4])
