@@ -50,6 +50,10 @@ def parse():
     p.add_argument("--restarts", type=int, default=30)
     p.add_argument("--rescored", type=int, default=30)
     p.add_argument("--seed", type=int, default=20260819)
+    p.add_argument("--pockets", type=int, default=1,
+                   help="configs[4]-style multi-pocket run: every step docks the batch against this many synthetic "
+                        "pockets (radius 8-14 A, spacing 0.375/0.5 A, distinct protein seeds); unit = pocket-ligand "
+                        "docks")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -223,6 +227,12 @@ def main():
     workload = (f"configs[1]: 3CL-sized synthetic pocket (65^3, 2400 protein atoms), drug-like ligands "
                 f"(~30 heavy / 5-7 rotors), k={args.restarts}, rescored={args.rescored}; "
                 f"{args.batch} ligands per GPU per step")
+    metric, unit = METRIC, UNIT
+    if args.pockets > 1:
+        workload = (f"configs[4]-style: {args.pockets} synthetic pockets (radius 8-14 A, spacing 0.375/0.5 A, distinct "
+                    f"protein seeds) x drug-like ligands (~30 heavy / 5-7 rotors), k={args.restarts}, "
+                    f"rescored={args.rescored}; {args.batch} ligands per GPU per step against every pocket")
+        metric, unit = "pocket-ligand docks+scored/sec", "docks/s"
 
     if args.impl == "reference":
         if rank != 0:
@@ -267,6 +277,11 @@ def main():
     t_setup = time.perf_counter()
     el, xyz = synth.synthetic_protein()
     pocket = api.build_pocket(el, xyz, [0.0, 0.0, 0.0], 12.0, 0.375, ctx)
+    pockets = [pocket]
+    for i in range(1, args.pockets):
+        e_i, x_i = synth.synthetic_protein(seed=args.seed + 101 * i)
+        radius = 8.0 + 6.0 * i / max(args.pockets - 1, 1)
+        pockets.append(api.build_pocket(e_i, x_i, [0.0, 0.0, 0.0], radius, 0.375 if i % 2 == 0 else 0.5, ctx))
     smi = api.synthetic_smiles(args.batch, seed=args.seed + 1 + 7919 * rank)
     ligs = api.prepare_ligand(smi, quantize=True, ctx=ctx, nthreads=threads)
     batch = pin_batch(LigandBatch(ligs))
@@ -289,8 +304,13 @@ def main():
             dist.barrier()
 
     def step(counters=False):
-        return api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False, out=out,
-                                        want_counters=counters)
+        if len(pockets) == 1:
+            return api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False, out=out,
+                                            want_counters=counters)
+        # multi-pocket (vs_dock_batch_multi): setup/flatten once, search +
+        # select per pocket (counters: one untimed run after the loop)
+        res, ms_, launches_, stages_ = api.dock_and_score_multi(pockets, batch, cfg, ctx)
+        return api.BatchResult(res[0], None, None, batch, ms_, launches_, None, stages_)
 
     for _ in range(args.warmup):
         flush.fill_(1)
@@ -312,13 +332,16 @@ def main():
         stages.append(last.stage_ms)
         launches += last.launches
     clk = clocks.stop()
+    if len(pockets) > 1:  # the roofline's work counters (first pocket), outside the timed region
+        last.counters = api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False,
+                                                 want_counters=True).counters
     tot_dev = sum(dev_ms) / 1e3
     tot_wall = sum(wall_s)
     if dist is not None:
         t = torch.tensor([tot_dev, tot_wall], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_dev, tot_wall = float(t[0]), float(t[1])
-    ligands_total = world * args.steps * batch.n_ligands
+    ligands_total = world * args.steps * batch.n_ligands * len(pockets)
     value = ligands_total / tot_dev
     e2e = ligands_total / tot_wall
     status = last.results["status"]
@@ -336,6 +359,8 @@ def main():
 
     # roofline of the dominant kernel (k_search) from the algorithmic FP64 work
     fl = split_flops(last.counters, batch, args.restarts)
+    if len(pockets) > 1:  # counters come from the first pocket: scale its work to all pockets (approximation)
+        fl = {key: v * len(pockets) for key, v in fl.items()}
     st_last = last.stage_ms
     peaks = measure_fp64_peak(local)
     search_s = st_last["search"] / 1e3
@@ -350,17 +375,18 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "unavailable", "sample": repr(e)}
     stage_mean = {k: float(np.mean([s[k] for s in stages])) for k in stages[0]}
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_dev / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload, "ligands_per_step": world * batch.n_ligands,
                    "pocket": "build_pocket(r=12 A, h=0.375 A) -> 65^3, synthetic protein seed 20260819",
                    "l2": "flushed between timed steps (256 MB device write)", "parallelism": f"replica x{world}",
                    "setup_s": round(setup_s, 2)},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world},
+        "e2e": {"value": e2e, "unit": unit, "h2d_bytes_per_step": int(h2d) * world * len(pockets),
+                "d2h_bytes_per_step": int(d2h) * world * len(pockets)},
         "gpu_launches": launches,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic_per_launch(batch.n_ligands),
+                     "frac": achieved / peak, "traffic": traffic_per_launch(batch.n_ligands * len(pockets)),
                      "traffic_unit": "bytes (DRAM read + write of the search stage of one step, ncu)",
                      "kernel": "k_search (initial_poses + local_search)",
                      "flops_per_launch": fl["search"], "launch_ms": st_last["search"],

@@ -227,6 +227,14 @@ vs_status vs_local_search_batch(vs_context *ctx, const vs_pocket *pocket, const 
                                 const vs_scoring_config *cfg, vs_pose *poses, double *angles,
                                 double *conformation, uint64_t *evals, int32_t *status_out);
 
+/* dock_and_score of every ligand of the batch against each of n_pockets
+ * pockets (BASELINE configs[4]: many pockets x one library).  The
+ * ligand-only stages (setup, flatten) run once per ligand, then the search
+ * and selection per pocket; results hold n_pockets x n_ligands entries,
+ * pocket-major, each identical to vs_dock_batch with that pocket. */
+vs_status vs_dock_batch_multi(vs_context *ctx, const vs_pocket *const *pockets, int32_t n_pockets,
+                              const vs_ligand_batch *batch, const vs_scoring_config *cfg, vs_dock_result *results);
+
 /* ---- measurement helper ------------------------------------------------- */
 /* Measured FP64 DADD ops/s, FP64 DFMA flop/s and FP32 FFMA flop/s of the
  * device (the roofline denominators of this CUDA-core path). */

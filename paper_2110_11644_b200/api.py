@@ -475,6 +475,24 @@ def dock_and_score_batch(pocket, ligands, config: ScoringConfig | None = None, c
                        counters[:b.n_ligands] if counters is not None else None, ctx.stage_timing())
 
 
+def dock_and_score_multi(pockets, ligands, config: ScoringConfig | None = None, ctx: Context | None = None,
+                         out=None):
+    """dock_and_score of every ligand against every pocket (BASELINE
+    configs[4]); ligand-only stages run once.  Returns (results array of shape
+    (n_pockets, n_ligands), device ms, launches, stage ms)."""
+    ctx = ctx or default_context()
+    dps = [_dev_pocket(p, ctx) for p in pockets]
+    b = _batch(ligands)
+    cfg = config or ScoringConfig()
+    res = out if out is not None else np.zeros((len(dps), max(b.n_ligands, 1)), dtype=abi.DOCK_RESULT_DTYPE)
+    arr = (C.c_void_p * len(dps))(*[d.handle for d in dps])
+    native.check(native.lib().vs_dock_batch_multi(ctx.handle, arr, len(dps), C.byref(b.desc()), C.byref(cfg),
+                                                  res.ctypes.data_as(C.POINTER(abi.DockResult))),
+                 "vs_dock_batch_multi")
+    ms, launches = ctx.last_timing()
+    return res[:, :b.n_ligands], ms, launches, ctx.stage_timing()
+
+
 def dock_and_score(pocket, ligand: Ligand, config: ScoringConfig | None = None,
                    ctx: Context | None = None) -> DockResult:
     """Single-ligand dock_and_score; raises ValueError where the reference

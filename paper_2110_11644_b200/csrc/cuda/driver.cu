@@ -71,6 +71,7 @@ struct vs_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evs[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_flat = nullptr;  // end of flatten (multi-pocket runs reuse evs[2..4] per pocket)
   double stage_ms[4] = {0, 0, 0, 0};  // setup, flatten, search, select
   double last_ms = 0.0;
   int last_launches = 0;
@@ -639,6 +640,7 @@ vs_status vs_context_create(int device, vs_context **out) {
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
   for (auto &e : ctx->evs) cudaEventCreate(&e);
+  cudaEventCreate(&ctx->ev_flat);
   ensure_lattice(device);
   *out = ctx;
   return VS_OK;
@@ -651,6 +653,7 @@ vs_status vs_context_destroy(vs_context *ctx) {
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   for (auto &e : ctx->evs) cudaEventDestroy(e);
+  cudaEventDestroy(ctx->ev_flat);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return VS_OK;
@@ -779,18 +782,22 @@ vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligan
   return vs_dock_batch_ex(ctx, pocket, batch, cfg, results, best_angles, best_conformation, nullptr);
 }
 
-vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
-                           const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
-                           double *best_conformation, uint64_t *counters) {
-  if (!ctx || !pocket || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+// The dock path over n_pockets pockets: setup and flatten run once per chunk
+// (they depend on the ligands only), then search + select per pocket.
+// results / best_angles / best_conformation / counters are arrays of
+// n_pockets pointers (entries may be NULL except results).
+static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int n_pockets,
+                           const vs_ligand_batch *batch, const vs_scoring_config *cfg, vs_dock_result *const *results_p,
+                           double *const *best_angles_p, double *const *best_conf_p, uint64_t *const *counters_p) {
   vs_status rc = check_cfg(cfg);
   if (rc) return rc;
-  if (pocket->device != ctx->device) return fail(VS_ERR_INVALID_ARGUMENT, "pocket lives on another device");
+  for (int pi = 0; pi < n_pockets; ++pi)
+    if (!pockets[pi] || !results_p[pi]) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+    else if (pockets[pi]->device != ctx->device) return fail(VS_ERR_INVALID_ARGUMENT, "pocket lives on another device");
   CtxLock lock(ctx);
   const int k = cfg->restarts;
   vsd::search_cfg sc{};
   if ((rc = upload_tables(ctx, *cfg, k, sc))) return rc;
-  const vsd::pocket_dev pd = pocket->dev();
   ctx->last_launches = 0;
   for (double &x : ctx->stage_ms) x = 0.0;
   float total_ms = 0.0f;
@@ -807,8 +814,6 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(ctx->best_ang.ensure(sizeof(double) * std::max(st.torsions, 1)));
     CUDA_TRY(ctx->best_conf.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
     CUDA_TRY(ctx->counters.ensure(sizeof(uint64_t) * 9 * std::max(st.n, 1)));
-    vsd::dock_out d{ctx->results.p, ctx->best_ang.as<double>(), ctx->best_conf.as<double>(),
-                    counters ? ctx->counters.as<unsigned long long>() : nullptr, f.sweeps};
     CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[0], ctx->stream));
     CUDA_TRY(vsd::launch_setup(st.b, k, ctx->stream));
@@ -819,8 +824,19 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
     if ((rc = flatten_buckets(ctx, st, cfg->flatten_max_sweeps, f))) return rc;
     CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev_flat, ctx->stream));
     CUDA_TRY(ctx->search_args.ensure(vsd::search_scratch_bytes(std::max(st.Nmax, 1), std::max(st.nmax, 1), std::max(st.mmax, 1), ctx->num_sms)));
     CUDA_TRY(cudaEventSynchronize(ctx->ev1));
+    float pocket_ms[2] = {0.0f, 0.0f};  // search, select summed over the pockets
+    for (int pi = 0; pi < n_pockets; ++pi) {
+    const vsd::pocket_dev pd = pockets[pi]->dev();
+    vs_dock_result *results = results_p[pi];
+    double *best_angles = best_angles_p ? best_angles_p[pi] : nullptr;
+    double *best_conformation = best_conf_p ? best_conf_p[pi] : nullptr;
+    uint64_t *counters = counters_p ? counters_p[pi] : nullptr;
+    vsd::dock_out d{ctx->results.p, ctx->best_ang.as<double>(), ctx->best_conf.as<double>(),
+                    counters ? ctx->counters.as<unsigned long long>() : nullptr, f.sweeps};
+    if (pi > 0) CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
     {
       // Size buckets: ligands grouped by how many 4-warp search CTAs per SM
       // their shared-memory footprint allows, each bucket launched with its
@@ -867,7 +883,7 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
     CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));
-    ctx->last_launches += 4;
+    ctx->last_launches += pi == 0 ? 4 : 2;
     CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,
                              ctx->stream));
     const int T0 = batch->torsion_offset[l0], A0 = batch->atom_offset[l0];
@@ -880,18 +896,48 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
     if (counters)
       CUDA_TRY(cudaMemcpyAsync(counters + 9 * static_cast<size_t>(l0), ctx->counters.p, sizeof(uint64_t) * 9 * st.n,
                                cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < 4; ++i) {
-      float ms = 0.0f;
-      cudaEventElapsedTime(&ms, ctx->evs[i], ctx->evs[i + 1]);
-      ctx->stage_ms[i] += ms;
+    if (n_pockets > 1) {  // per-pocket stage times (the events are reused by the next pocket)
+      CUDA_TRY(cudaEventSynchronize(ctx->evs[4]));
+      float a = 0.0f, b2 = 0.0f;
+      cudaEventElapsedTime(&a, ctx->evs[2], ctx->evs[3]);
+      cudaEventElapsedTime(&b2, ctx->evs[3], ctx->evs[4]);
+      pocket_ms[0] += a;
+      pocket_ms[1] += b2;
     }
+    }  // pockets
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    float st_ms[4] = {0, 0, 0, 0};
+    cudaEventElapsedTime(&st_ms[0], ctx->evs[0], ctx->evs[1]);
+    cudaEventElapsedTime(&st_ms[1], ctx->evs[1], ctx->ev_flat);
+    if (n_pockets > 1) {
+      st_ms[2] = pocket_ms[0];
+      st_ms[3] = pocket_ms[1];
+    } else {
+      cudaEventElapsedTime(&st_ms[2], ctx->evs[2], ctx->evs[3]);
+      cudaEventElapsedTime(&st_ms[3], ctx->evs[3], ctx->evs[4]);
+    }
+    for (int i = 0; i < 4; ++i) ctx->stage_ms[i] += st_ms[i];
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, ctx->evs[0], ctx->evs[4]);
     total_ms += ms;
   }
   ctx->last_ms = total_ms;
   return VS_OK;
+}
+
+vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_ligand_batch *batch,
+                           const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
+                           double *best_conformation, uint64_t *counters) {
+  if (!ctx || !pocket || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  return dock_impl(ctx, &pocket, 1, batch, cfg, &results, &best_angles, &best_conformation, &counters);
+}
+
+vs_status vs_dock_batch_multi(vs_context *ctx, const vs_pocket *const *pockets, int32_t n_pockets,
+                              const vs_ligand_batch *batch, const vs_scoring_config *cfg, vs_dock_result *results) {
+  if (!ctx || !pockets || n_pockets < 1 || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<vs_dock_result *> res(static_cast<size_t>(n_pockets));
+  for (int p = 0; p < n_pockets; ++p) res[p] = results + static_cast<size_t>(p) * batch->n_ligands;
+  return dock_impl(ctx, pockets, n_pockets, batch, cfg, res.data(), nullptr, nullptr, nullptr);
 }
 
 vs_status vs_field_values(vs_context *ctx, const vs_pocket *pocket, int64_t n, const double *xyz, double *out) {

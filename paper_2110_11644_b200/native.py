@@ -42,6 +42,7 @@ SIGNATURES = {
     "vs_pocket_destroy": (C.c_int, [_vp]),
     "vs_dock_batch": (C.c_int, [_vp, _vp, _LB, _CF, _DR, _d, _d]),
     "vs_dock_batch_ex": (C.c_int, [_vp, _vp, _LB, _CF, _DR, _d, _d, _u64]),
+    "vs_dock_batch_multi": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, _LB, _CF, _DR]),
     "vs_context_stage_timing": (C.c_int, [_vp, _d]),
     "vs_field_values": (C.c_int, [_vp, _vp, C.c_int64, _d, _d]),
     "vs_geo_score_batch": (C.c_int, [_vp, _vp, _LB, _d, _d, _u64]),

@@ -235,6 +235,20 @@ def test_dock_bit_exact_config_variations(env, kw):
     assert np.array_equal(got.counters, want["counters"]), kw
 
 
+def test_dock_multi_pocket_equals_single(env):
+    """vs_dock_batch_multi (configs[4]: flatten once, search per pocket)
+    returns exactly the per-pocket vs_dock_batch results."""
+    ctx, pocket, host, b = env
+    sub = LigandBatch(b.ligands[:32])
+    el, xyz = synth.synthetic_protein(seed=99)
+    p2 = api.build_pocket(el, xyz, [0.0, 0.0, 0.0], 9.0, 0.5, ctx)
+    cfg = abi.ScoringConfig(restarts=6, rescored=4)
+    multi, _, _, _ = api.dock_and_score_multi([pocket, p2, pocket], sub, cfg, ctx)
+    for j, pk in enumerate([pocket, p2, pocket]):
+        one = api.dock_and_score_batch(pk, sub, cfg, ctx, want_conformation=False).results
+        assert np.array_equal(multi[j].view(np.uint8), one.view(np.uint8)), j
+
+
 def test_dock_default_config_256_restarts(env):
     ctx, pocket, host, b = env
     sub = LigandBatch(b.ligands[:4])
