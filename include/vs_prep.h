@@ -58,6 +58,12 @@ int32_t vs_bridge_bonds(const vs_ligand_batch *b, int32_t i, uint8_t *bridge_out
  * returns the number of bytes used, or -1 if cap is too small. */
 int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, int32_t max_heavy, int32_t min_rot,
                         int32_t max_rot, char *buf, int64_t cap);
+/* The same with a grammar choice: 0 = the drug-like grammar above
+ * (vs_synth_smiles), 1 = wide (adds larger rigid fused systems and flexible
+ * chain linkers/tails, for the BASELINE configs[2] size sweep).  Returns -2
+ * when the window is unreachable. */
+int64_t vs_synth_smiles_ex(int32_t n, uint64_t seed, int32_t min_heavy, int32_t max_heavy, int32_t min_rot,
+                           int32_t max_rot, int32_t grammar, char *buf, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -267,11 +267,11 @@ def embed_ligand(smiles: str) -> Ligand:
     return prepare_smiles([smiles], mode=1)[0]
 
 
-def synthetic_smiles(n: int, seed: int = 20260819, heavy=(26, 34), rot=(5, 7)) -> list:
+def synthetic_smiles(n: int, seed: int = 20260819, heavy=(26, 34), rot=(5, 7), grammar: int = 0) -> list:
     cap = max(256, n * 96)
     while True:
         buf = C.create_string_buffer(cap)
-        used = native.lib().vs_synth_smiles(n, seed, heavy[0], heavy[1], rot[0], rot[1], buf, cap)
+        used = native.lib().vs_synth_smiles_ex(n, seed, heavy[0], heavy[1], rot[0], rot[1], grammar, buf, cap)
         if used == -2:
             raise ValueError("requested heavy/rotor window is unreachable")
         if used >= 0:

@@ -77,6 +77,20 @@ const RingUnit kRings[] = {
     {"C%CCc&ccccc&C%", {"C%CCc&cc(ccc&C%)", "C%CCc&c(cccc&C%)", "C%CC(c&ccccc&C%)"}, "C%CCc&cc($)c(cc&C%)"},
     {"c%ccc&ncccc&c%", {"c%ccc&ncc(cc&c%)", "c%ccc&nc(ccc&c%)", "c%cc(c&ncccc&c%)"}, "c%cc($)c&ncc(cc&c%)"},
 };
+// Wide grammar (vs_synth_smiles_ex grammar 1, the configs[2] size sweep):
+// larger rigid fused systems ('^' = third ring digit) for heavy, low-rotor
+// ligands, and flexible chain linkers / tails for small, many-rotor ones.
+const RingUnit kRingsWide[] = {
+    {"c%ccc&cc^ccccc^cc&c%", {"c%ccc&cc^ccc(cc^cc&c%)", "c%ccc&cc^cccc(c^cc&c%)", "c%cc(c&cc^ccccc^cc&c%)"},
+     "c%cc($)c&cc^ccc(cc^cc&c%)"},
+    {"c%ccc&c(c%)ccc^ccccc&^", {"c%ccc&c(c%)ccc^cccc(c&^)", "c%cc(c&c(c%)ccc^ccccc&^)", "c%ccc&c(c%)cc(c^ccccc&^)"},
+     "c%cc($)c&c(c%)ccc^cccc(c&^)"},
+    {"C%CCC&CCCCC&C%", {"C%CCC&CC(CCC&C%)", "C%CCC&C(CCCC&C%)", "C%CC(C&CCCCC&C%)"}, "C%CC($)C&CC(CCC&C%)"},
+};
+const char *kLinkersWide[] = {"CCCC", "CCCCC", "OCCO", "CCOCC", "CCCCCC", "CCNCC", "C", "CC", "", "O"};
+const char *kTailsWide[] = {"CCCCC", "CCCCCCC", "OCCCC", "CCCCOC", "F", "Cl", "C", "Br"};
+const char *kSubstWide[] = {"F", "Cl", "Br", "C", "CCCC", "OCCC"};
+
 const char *kLinkers[] = {"",   "",    "C",      "CC",   "O",     "N",  "C(=O)N", "NC(=O)", "C(=O)O", "OC",
                           "CO", "S",   "CN",     "NC",   "C(=O)", "CC(=O)N", "OCC", "CCO", "C(C)N", "CCN"};
 const char *kSubst[] = {"F", "Cl", "Br", "C", "O", "N", "OC", "C(=O)O", "C#N", "C(F)(F)F", "N(C)C", "CC", "C(=O)N", "OCC"};
@@ -89,6 +103,8 @@ std::string with_digit(const char *tmpl, int digit, const char *subst) {
       out += static_cast<char>('0' + digit);
     else if (*p == '&')
       out += static_cast<char>('0' + digit + 1);
+    else if (*p == '^')
+      out += static_cast<char>('0' + digit + 2);
     else if (*p == '$')
       out += subst;
     else
@@ -121,12 +137,41 @@ std::string candidate(Xoshiro &rng, int rmin, int rmax) {
   return s;
 }
 
+template <typename T, size_t N>
+constexpr int count_of(const T (&)[N]) {
+  return static_cast<int>(N);
+}
+
+std::string candidate_wide(Xoshiro &rng, int rmin, int rmax) {
+  std::string s;
+  if (rng.below(2) == 0) s += kTailsWide[rng.below(count_of(kTailsWide))];
+  const int rings = rmin + rng.below(rmax - rmin + 1);
+  for (int r = 0; r < rings; ++r) {
+    const bool big = rng.below(3) == 0;
+    const RingUnit &u = big ? kRingsWide[rng.below(count_of(kRingsWide))] : kRings[rng.below(count_of(kRings))];
+    const bool last = r + 1 == rings;
+    const bool tail_after = last && rng.below(2) == 0;
+    if (last && !tail_after) {
+      s += with_digit(u.terminal, 1, "");
+    } else if (rng.below(3) == 0) {
+      s += with_digit(u.subst, 1, kSubstWide[rng.below(count_of(kSubstWide))]);
+    } else {
+      s += with_digit(u.exits[rng.below(3)], 1, "");
+    }
+    if (!last)
+      s += rng.below(2) ? kLinkersWide[rng.below(count_of(kLinkersWide))] : kLinkers[rng.below(count_of(kLinkers))];
+    else if (tail_after)
+      s += kTailsWide[rng.below(count_of(kTailsWide))];
+  }
+  return s;
+}
+
 }  // namespace
 
 // Blocks of 256 accepted SMILES, each from its own xoshiro stream
 // (seed, block) -- deterministic for any thread count.
-extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, int32_t max_heavy,
-                                   int32_t min_rot, int32_t max_rot, char *buf, int64_t cap) {
+extern "C" int64_t vs_synth_smiles_ex(int32_t n, uint64_t seed, int32_t min_heavy, int32_t max_heavy,
+                                      int32_t min_rot, int32_t max_rot, int32_t grammar, char *buf, int64_t cap) {
   constexpr int kBlock = 256;
   const int nblocks = (n + kBlock - 1) / kBlock;
   std::vector<std::vector<std::string>> blocks(static_cast<size_t>(nblocks));
@@ -137,8 +182,8 @@ extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, 
       Xoshiro rng(seed * 0x9e3779b97f4a7c15ULL + static_cast<uint64_t>(bi) + 1);
       const int want = std::min(kBlock, n - bi * kBlock);
       // ring units scale with the requested size (2-3 for ~30 heavy atoms)
-      const int rmin = std::max(1, min_heavy / 13);
-      const int rmax = std::max(rmin + 1, max_heavy / 11);
+      const int rmin = grammar ? 1 : std::max(1, min_heavy / 13);
+      const int rmax = grammar ? std::max(2, max_heavy / 8) : std::max(rmin + 1, max_heavy / 11);
       auto &out = blocks[static_cast<size_t>(bi)];
       int64_t tries = 0;
       while (static_cast<int>(out.size()) < want) {
@@ -148,7 +193,7 @@ extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, 
           unreachable = true;
           return;
         }
-        std::string s = candidate(rng, rmin, rmax);
+        std::string s = grammar ? candidate_wide(rng, rmin, rmax) : candidate(rng, rmin, rmax);
         int heavy = 0, rot = 0;
         if (!vsprep_internal::counts(s, &heavy, &rot)) continue;
         if (heavy < min_heavy || heavy > max_heavy || rot < min_rot || rot > max_rot) continue;
@@ -171,4 +216,9 @@ extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, 
       used += need;
     }
   return used;
+}
+
+extern "C" int64_t vs_synth_smiles(int32_t n, uint64_t seed, int32_t min_heavy, int32_t max_heavy, int32_t min_rot,
+                                   int32_t max_rot, char *buf, int64_t cap) {
+  return vs_synth_smiles_ex(n, seed, min_heavy, max_heavy, min_rot, max_rot, 0, buf, cap);
 }

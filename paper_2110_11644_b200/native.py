@@ -70,6 +70,8 @@ SIGNATURES = {
     "vs_bridge_bonds": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint8)]),
     "vs_synth_smiles": (C.c_int64, [C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_char_p, C.c_int64]),
+    "vs_synth_smiles_ex": (C.c_int64, [C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_char_p, C.c_int64]),
 }
 
 _lib = None

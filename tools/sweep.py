@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=64)
     ap.add_argument("--heavy", default="10,20,30,40,50,60,70,80")
     ap.add_argument("--rot", default="0,3,6,9,12,15")
+    ap.add_argument("--grammar", type=int, default=1, help="synthetic SMILES grammar: 0 drug-like, 1 wide")
     args = ap.parse_args()
     ctx = api.default_context(0)
     el, xyz = synth.synthetic_protein()
@@ -48,7 +49,7 @@ def main():
             cell = {"heavy": n, "rotors": m}
             try:
                 smi = api.synthetic_smiles(args.per_cell, seed=20260819 + 1000 * n + m, heavy=(max(1, n - 2), n + 2),
-                                           rot=(m, m))
+                                           rot=(m, m), grammar=args.grammar)
             except ValueError:
                 print(json.dumps({**cell, "skipped": "generator cannot reach this (heavy, rotor) window"}), flush=True)
                 continue
