@@ -54,6 +54,9 @@ def parse():
                    help="configs[4]-style multi-pocket run: every step docks the batch against this many synthetic "
                         "pockets (radius 8-14 A, spacing 0.375/0.5 A, distinct protein seeds); unit = pocket-ligand "
                         "docks")
+    p.add_argument("--input", default="soa", choices=["soa", "records"],
+                   help="soa: the prepared batch (vs_ligand_batch) is staged each step; records: the batch as an "
+                        ".xslb record stream, decoded and docked on the GPU each step (vs_dock_records)")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -303,7 +306,16 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    records = offsets = None
+    if args.input == "records":
+        records = pinned_like(np.frombuffer(api.encode_records(batch.ligands, smi), dtype=np.uint8))
+        offsets = api.frame_records(records.tobytes())
+        h2d = records.nbytes + offsets.nbytes
+
     def step(counters=False):
+        if records is not None:
+            res, rst, ms_, stages_ = api.dock_records(pockets, records, offsets, cfg, ctx)
+            return api.BatchResult(res[0], None, None, batch, ms_, ctx.last_timing()[1] + 1, None, stages_)
         if len(pockets) == 1:
             return api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False, out=out,
                                             want_counters=counters)
@@ -332,7 +344,7 @@ def main():
         stages.append(last.stage_ms)
         launches += last.launches
     clk = clocks.stop()
-    if len(pockets) > 1:  # the roofline's work counters (first pocket), outside the timed region
+    if len(pockets) > 1 or records is not None:  # the roofline's work counters, outside the timed region
         last.counters = api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False,
                                                  want_counters=True).counters
     tot_dev = sum(dev_ms) / 1e3

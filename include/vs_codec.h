@@ -54,6 +54,17 @@ int32_t vs_xslb_frame(const uint8_t *bytes, int64_t size, int64_t start, int32_t
 vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, int64_t size, const int64_t *offsets, int32_t n,
                             vs_ligand_set **out);
 
+/* Decode + dock in one call (the pipeline's CUDA worker: decode_record then
+ * dock_and_score per record, pipeline.cpp:206-244): the records are framed on
+ * the host, decoded on the GPU straight into the dock path's device inputs
+ * (no host round trip of the decoded batch) and docked against each of the
+ * n_pockets pockets.  results: n_pockets x n entries, pocket-major; a record
+ * that fails to decode gets status VS_LIG_BAD_RECORD and its
+ * vs_record_status in record_status (may be NULL). */
+vs_status vs_dock_records(vs_context *ctx, const vs_pocket *const *pockets, int32_t n_pockets, const uint8_t *bytes,
+                          int64_t size, const int64_t *offsets, int32_t n, const vs_scoring_config *cfg,
+                          vs_dock_result *results, int32_t *record_status);
+
 /* encode_record (binary_codec.cpp:129-163) of every ligand of a batch, back to
  * back, coordinates truncated to f32 (host).  names may be NULL (empty
  * names).  Returns the bytes written, or -(bytes needed) if cap is too small. */

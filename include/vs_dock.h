@@ -54,7 +54,8 @@ typedef enum vs_ligand_status {
   VS_LIG_BAD_TORSION = 3,     /* torsion bond / atom index out of range         */
   VS_LIG_NO_HEAVY = 4,        /* "no heavy atoms" (transform.cpp:111)           */
   VS_LIG_TOO_LARGE = 5,       /* exceeds VS_MAX_* device limits (see below)     */
-  VS_LIG_NONFINITE = 6        /* non-finite best score (pipeline.cpp:224-229)   */
+  VS_LIG_NONFINITE = 6,       /* non-finite best score (pipeline.cpp:224-229)   */
+  VS_LIG_BAD_RECORD = 7       /* vs_dock_records: the record failed to decode   */
 } vs_ligand_status;
 
 /* Device limits of the sm_100a kernels (per ligand).  The reference caps

@@ -26,6 +26,7 @@ VS_LIG_BAD_TORSION = 3
 VS_LIG_NO_HEAVY = 4
 VS_LIG_TOO_LARGE = 5
 VS_LIG_NONFINITE = 6
+VS_LIG_BAD_RECORD = 7
 
 LIGAND_STATUS_NAMES = {
     VS_LIG_OK: "ok",
@@ -35,6 +36,7 @@ LIGAND_STATUS_NAMES = {
     VS_LIG_NO_HEAVY: "no heavy atoms",
     VS_LIG_TOO_LARGE: "ligand exceeds device limits",
     VS_LIG_NONFINITE: "non-finite score",
+    VS_LIG_BAD_RECORD: "record failed to decode",
 }
 
 VS_MAX_ATOMS = 256

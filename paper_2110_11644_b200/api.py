@@ -493,6 +493,29 @@ def dock_and_score_multi(pockets, ligands, config: ScoringConfig | None = None, 
     return res[:, :b.n_ligands], ms, launches, ctx.stage_timing()
 
 
+def dock_records(pockets, data: bytes, offsets=None, config: ScoringConfig | None = None, ctx: Context | None = None):
+    """Decode + dock the records of an .xslb byte stream on the GPU without a
+    host round trip (vs_dock_records).  Returns (results of shape
+    (n_pockets, n_records), record status, device ms, stage ms)."""
+    ctx = ctx or default_context()
+    dps = [_dev_pocket(p, ctx) for p in pockets]
+    if offsets is None:
+        offsets = frame_records(data)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    n = len(offs)
+    buf = np.frombuffer(data, dtype=np.uint8)
+    cfg = config or ScoringConfig()
+    res = np.zeros((len(dps), max(n, 1)), dtype=abi.DOCK_RESULT_DTYPE)
+    rst = np.zeros(max(n, 1), dtype=np.int32)
+    arr = (C.c_void_p * len(dps))(*[d.handle for d in dps])
+    native.check(native.lib().vs_dock_records(ctx.handle, arr, len(dps), abi.ptr(buf, C.c_uint8), len(data),
+                                              abi.ptr(offs, C.c_int64), n, C.byref(cfg),
+                                              res.ctypes.data_as(C.POINTER(abi.DockResult)),
+                                              abi.ptr(rst, C.c_int32)), "vs_dock_records")
+    ms, _ = ctx.last_timing()
+    return res[:, :n], rst[:n], ms, ctx.stage_timing()
+
+
 def dock_and_score(pocket, ligand: Ligand, config: ScoringConfig | None = None,
                    ctx: Context | None = None) -> DockResult:
     """Single-ligand dock_and_score; raises ValueError where the reference

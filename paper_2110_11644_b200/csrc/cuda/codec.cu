@@ -45,6 +45,7 @@ struct decode_args {
   uint16_t *ba, *bb, *tbond, *rslots;
   int *rcount;  // per torsion: right-set size
   int *status;  // per record: in = host framing status, out = decode status
+  int *nheavy;  // per record: heavy atoms (NULL: not needed)
 };
 
 // Reachability from `start` over the record's bonds, bond `skip` removed,
@@ -107,6 +108,12 @@ __global__ void __launch_bounds__(32 * kDecWarps) k_decode(decode_args A) {
     if (code > 10u) err = VS_REC_BAD_ELEMENT;
     else if (!isfinite(x) || !isfinite(y) || !isfinite(z)) err = VS_REC_NONFINITE;
     if (err && first == ~0ull) first = ((unsigned long long)i << 4) | (unsigned long long)err;
+  }
+  if (A.nheavy) {
+    int hc = 0;
+    for (int i = lane; i < na; i += 32) hc += (rd8(pa + 14 * (size_t)i + 13) & 1u) ? 1 : 0;
+    hc = __reduce_add_sync(0xffffffffu, hc);
+    if (lane == 0) A.nheavy[r] = hc;
   }
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned long long o = __shfl_xor_sync(0xffffffffu, first, off);
@@ -171,15 +178,33 @@ __global__ void __launch_bounds__(32 * kDecWarps) k_decode(decode_args A) {
   if (lane == 0) A.status[r] = st;
 }
 
+// Right sets from the padded decode slots into the dock path's compact
+// right_atoms (thread per torsion; failed records have count 0).
+__global__ void k_compact_right(const uint16_t *slots, const int64_t *rs_off, const int *rcount, const int *right_off,
+                                int n_tors, uint16_t *right_atoms) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tors) return;
+  const uint16_t *src = slots + rs_off[t];
+  uint16_t *dst = right_atoms + right_off[t];
+  for (int i = 0; i < rcount[t]; ++i) dst[i] = src[i];
+}
+
 }  // namespace
+
+cudaError_t launch_compact_right(const uint16_t *slots, const int64_t *rs_off, const int *rcount, const int *right_off,
+                                 int n_tors, uint16_t *right_atoms, cudaStream_t s) {
+  if (n_tors <= 0) return cudaSuccess;
+  k_compact_right<<<(n_tors + 127) / 128, 128, 0, s>>>(slots, rs_off, rcount, right_off, n_tors, right_atoms);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_decode(const uint8_t *bytes, const int64_t *offs, int n, const int *atom_off, const int *bond_off,
                           const int *tors_off, const int64_t *rs_off, double *xyz, uint8_t *elem, uint8_t *heavy,
                           uint8_t *border, uint16_t *ba, uint16_t *bb, uint16_t *tbond, uint16_t *rslots, int *rcount,
-                          int *status, cudaStream_t s) {
+                          int *status, cudaStream_t s, int *nheavy) {
   if (n <= 0) return cudaSuccess;
   decode_args A{bytes, offs, n, atom_off, bond_off, tors_off, rs_off, xyz, elem, heavy, border,
-                ba, bb, tbond, rslots, rcount, status};
+                ba, bb, tbond, rslots, rcount, status, nheavy};
   k_decode<<<(n + kDecWarps - 1) / kDecWarps, 32 * kDecWarps, 0, s>>>(A);
   return cudaGetLastError();
 }

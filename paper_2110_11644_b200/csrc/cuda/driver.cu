@@ -786,26 +786,36 @@ vs_status vs_dock_batch(vs_context *ctx, const vs_pocket *pocket, const vs_ligan
 // (they depend on the ligands only), then search + select per pocket.
 // results / best_angles / best_conformation / counters are arrays of
 // n_pockets pointers (entries may be NULL except results).
+static vs_status check_pockets(const vs_context *ctx, const vs_pocket *const *pockets, int n_pockets) {
+  for (int pi = 0; pi < n_pockets; ++pi)
+    if (!pockets[pi]) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+    else if (pockets[pi]->device != ctx->device) return fail(VS_ERR_INVALID_ARGUMENT, "pocket lives on another device");
+  return VS_OK;
+}
+
+// `pre`: a batch already staged on the device (vs_dock_records); else the
+// host batch is staged chunk by chunk.  The caller holds the context lock.
 static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int n_pockets,
                            const vs_ligand_batch *batch, const vs_scoring_config *cfg, vs_dock_result *const *results_p,
-                           double *const *best_angles_p, double *const *best_conf_p, uint64_t *const *counters_p) {
+                           double *const *best_angles_p, double *const *best_conf_p, uint64_t *const *counters_p,
+                           Staged *pre = nullptr) {
   vs_status rc = check_cfg(cfg);
   if (rc) return rc;
+  if ((rc = check_pockets(ctx, pockets, n_pockets))) return rc;
   for (int pi = 0; pi < n_pockets; ++pi)
-    if (!pockets[pi] || !results_p[pi]) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
-    else if (pockets[pi]->device != ctx->device) return fail(VS_ERR_INVALID_ARGUMENT, "pocket lives on another device");
-  CtxLock lock(ctx);
+    if (!results_p[pi]) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
   const int k = cfg->restarts;
   vsd::search_cfg sc{};
   if ((rc = upload_tables(ctx, *cfg, k, sc))) return rc;
   ctx->last_launches = 0;
   for (double &x : ctx->stage_ms) x = 0.0;
   float total_ms = 0.0f;
-  const std::vector<int> cut = chunks(batch, k, size_t(12) << 30);
+  const std::vector<int> cut = pre ? std::vector<int>{0, pre->n} : chunks(batch, k, size_t(12) << 30);
   for (size_t ci = 0; ci + 1 < cut.size(); ++ci) {
     const int l0 = cut[ci], l1 = cut[ci + 1];
-    Staged st;
-    if ((rc = stage(ctx, batch, l0, l1, st))) return rc;
+    Staged st_local;
+    Staged &st = pre ? *pre : st_local;
+    if (!pre && (rc = stage(ctx, batch, l0, l1, st))) return rc;
     vsd::flat_out f{};
     vsd::item_out o{};
     if ((rc = ensure_flat(ctx, st, f))) return rc;
@@ -886,7 +896,7 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
     ctx->last_launches += pi == 0 ? 4 : 2;
     CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,
                              ctx->stream));
-    const int T0 = batch->torsion_offset[l0], A0 = batch->atom_offset[l0];
+    const int T0 = batch ? batch->torsion_offset[l0] : 0, A0 = batch ? batch->atom_offset[l0] : 0;
     if (best_angles && st.torsions)
       CUDA_TRY(cudaMemcpyAsync(best_angles + T0, ctx->best_ang.p, sizeof(double) * st.torsions, cudaMemcpyDeviceToHost,
                                ctx->stream));
@@ -929,6 +939,7 @@ vs_status vs_dock_batch_ex(vs_context *ctx, const vs_pocket *pocket, const vs_li
                            const vs_scoring_config *cfg, vs_dock_result *results, double *best_angles,
                            double *best_conformation, uint64_t *counters) {
   if (!ctx || !pocket || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
   return dock_impl(ctx, &pocket, 1, batch, cfg, &results, &best_angles, &best_conformation, &counters);
 }
 
@@ -937,6 +948,7 @@ vs_status vs_dock_batch_multi(vs_context *ctx, const vs_pocket *const *pockets, 
   if (!ctx || !pockets || n_pockets < 1 || !batch || !results) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
   std::vector<vs_dock_result *> res(static_cast<size_t>(n_pockets));
   for (int p = 0; p < n_pockets; ++p) res[p] = results + static_cast<size_t>(p) * batch->n_ligands;
+  CtxLock lock(ctx);
   return dock_impl(ctx, pockets, n_pockets, batch, cfg, res.data(), nullptr, nullptr, nullptr);
 }
 
@@ -1179,19 +1191,16 @@ const char *record_error(int st) {
 
 uint32_t rd16h(const uint8_t *p) { return (uint32_t)p[0] | ((uint32_t)p[1] << 8); }
 
-}  // namespace
-
-// decode_record (binary_codec.cpp:165-222) of n records on the GPU: the host
-// reads only the framing (marker, length, name, counts) to size the outputs;
-// payloads, validation and torsion partitions run in k_decode (codec.cu).
-extern "C" vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, int64_t size, const int64_t *offsets,
-                                       int32_t n, vs_ligand_set **out) {
-  if (!ctx || !out || n < 0 || (n > 0 && (!bytes || !offsets))) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
-  CtxLock lock(ctx);
-  auto *set = new vs_ligand_set;
-  const size_t N = static_cast<size_t>(n);
-  std::vector<int32_t> st(N, VS_REC_OK), na(N, 0), nb(N, 0), nt(N, 0);
-  set->names.assign(N, std::string());
+// Host side of the record decode: per record, the framing checks of
+// decode_record (marker, truncation, payload length) and the counts.
+void frame_host(const uint8_t *bytes, int64_t size, const int64_t *offsets, size_t N, std::vector<int32_t> &st,
+                std::vector<int32_t> &na, std::vector<int32_t> &nb, std::vector<int32_t> &nt,
+                std::vector<std::string> *names) {
+  st.assign(N, VS_REC_OK);
+  na.assign(N, 0);
+  nb.assign(N, 0);
+  nt.assign(N, 0);
+  if (names) names->assign(N, std::string());
   for (size_t r = 0; r < N; ++r) {
     const int64_t at = offsets[r];
     if (at < 0 || at + 2 > size || bytes[at] != 0xD0 || bytes[at + 1] != 0xC5) {
@@ -1220,11 +1229,26 @@ extern "C" vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, in
       st[r] = VS_REC_LENGTH_MISMATCH;
       continue;
     }
-    set->names[r].assign(reinterpret_cast<const char *>(bytes + at + 8), name_len);
+    if (names) (*names)[r].assign(reinterpret_cast<const char *>(bytes + at + 8), name_len);
     na[r] = static_cast<int32_t>(a);
     nb[r] = static_cast<int32_t>(b);
     nt[r] = static_cast<int32_t>(t);
   }
+}
+
+}  // namespace
+
+// decode_record (binary_codec.cpp:165-222) of n records on the GPU: the host
+// reads only the framing (marker, length, name, counts) to size the outputs;
+// payloads, validation and torsion partitions run in k_decode (codec.cu).
+extern "C" vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, int64_t size, const int64_t *offsets,
+                                       int32_t n, vs_ligand_set **out) {
+  if (!ctx || !out || n < 0 || (n > 0 && (!bytes || !offsets))) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  CtxLock lock(ctx);
+  auto *set = new vs_ligand_set;
+  const size_t N = static_cast<size_t>(n);
+  std::vector<int32_t> st, na, nb, nt;
+  frame_host(bytes, size, offsets, N, st, na, nb, nt, &set->names);
   std::vector<int32_t> aoff(N + 1, 0), boff(N + 1, 0), toff(N + 1, 0);
   for (size_t r = 0; r < N; ++r) {
     aoff[r + 1] = aoff[r] + na[r];
@@ -1334,4 +1358,147 @@ extern "C" vs_status vs_decode_records(vs_context *ctx, const uint8_t *bytes, in
   }
   *out = set;
   return VS_OK;
+}
+
+// The pipeline's decode -> dock without a host round trip of the decoded
+// batch: records are framed on the host, decoded by k_decode straight into
+// the dock path's device input arrays, and docked against every pocket.
+extern "C" vs_status vs_dock_records(vs_context *ctx, const vs_pocket *const *pockets, int32_t n_pockets,
+                                     const uint8_t *bytes, int64_t size, const int64_t *offsets, int32_t n,
+                                     const vs_scoring_config *cfg, vs_dock_result *results, int32_t *record_status) {
+  if (!ctx || !pockets || n_pockets < 1 || n < 0 || !results || (n > 0 && (!bytes || !offsets)))
+    return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  vs_status rc = check_cfg(cfg);
+  if (rc) return rc;
+  if ((rc = check_pockets(ctx, pockets, n_pockets))) return rc;
+  CtxLock lock(ctx);
+  const size_t N = static_cast<size_t>(n);
+  std::vector<int32_t> st, na, nb, nt;
+  frame_host(bytes, size, offsets, N, st, na, nb, nt, nullptr);
+  Staged sg;
+  sg.n = n;
+  sg.atom_off.assign(N + 1, 0);
+  sg.bond_off.assign(N + 1, 0);
+  sg.tors_off.assign(N + 1, 0);
+  for (size_t r = 0; r < N; ++r) {
+    sg.atom_off[r + 1] = sg.atom_off[r] + na[r];
+    sg.bond_off[r + 1] = sg.bond_off[r] + nb[r];
+    sg.tors_off[r + 1] = sg.tors_off[r] + nt[r];
+  }
+  sg.atoms = sg.atom_off[N];
+  sg.torsions = sg.tors_off[N];
+  const size_t atoms = sg.atoms, bonds = sg.bond_off[N], tors = sg.torsions;
+  std::vector<int64_t> rsoff(tors + 1, 0);
+  for (size_t r = 0; r < N; ++r)
+    for (int q = 0; q < nt[r]; ++q) rsoff[sg.tors_off[r] + q + 1] = rsoff[sg.tors_off[r] + q] + na[r];
+  cudaStream_t s = ctx->stream;
+  if ((rc = h2d(ctx->dec_bytes, bytes, static_cast<size_t>(std::max<int64_t>(size, 0)), s))) return rc;
+  if ((rc = h2d(ctx->dec_offs, offsets, N, s))) return rc;
+  if ((rc = h2d(ctx->atom_off, sg.atom_off.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->bond_off, sg.bond_off.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->tors_off, sg.tors_off.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->dec_rsoff, rsoff.data(), rsoff.size(), s))) return rc;
+  if ((rc = h2d(ctx->dec_status, st.data(), N, s))) return rc;
+  CUDA_TRY(ctx->xyz.ensure(sizeof(double) * 3 * std::max<size_t>(atoms, 1)));
+  CUDA_TRY(ctx->elem.ensure(std::max<size_t>(atoms, 1)));
+  CUDA_TRY(ctx->heavy.ensure(std::max<size_t>(atoms, 1)));
+  CUDA_TRY(ctx->dec_order.ensure(std::max<size_t>(bonds, 1)));
+  CUDA_TRY(ctx->bond_a.ensure(sizeof(uint16_t) * std::max<size_t>(bonds, 1)));
+  CUDA_TRY(ctx->bond_b.ensure(sizeof(uint16_t) * std::max<size_t>(bonds, 1)));
+  CUDA_TRY(ctx->tors_bond.ensure(sizeof(uint16_t) * std::max<size_t>(tors, 1)));
+  CUDA_TRY(ctx->dec_rslots.ensure(sizeof(uint16_t) * std::max<int64_t>(rsoff.back(), 1)));
+  CUDA_TRY(ctx->dec_rcount.ensure(sizeof(int) * std::max<size_t>(tors, 1)));
+  CUDA_TRY(ctx->aux3.ensure(sizeof(int) * std::max<size_t>(N, 1)));  // heavy atoms per record
+  CUDA_TRY(vsd::launch_decode(ctx->dec_bytes.as<uint8_t>(), ctx->dec_offs.as<int64_t>(), n, ctx->atom_off.as<int>(),
+                              ctx->bond_off.as<int>(), ctx->tors_off.as<int>(), ctx->dec_rsoff.as<int64_t>(),
+                              ctx->xyz.as<double>(), ctx->elem.as<uint8_t>(), ctx->heavy.as<uint8_t>(),
+                              ctx->dec_order.as<uint8_t>(), ctx->bond_a.as<uint16_t>(), ctx->bond_b.as<uint16_t>(),
+                              ctx->tors_bond.as<uint16_t>(), ctx->dec_rslots.as<uint16_t>(), ctx->dec_rcount.as<int>(),
+                              ctx->dec_status.as<int>(), s, ctx->aux3.as<int>()));
+  std::vector<int> rcount(tors), nh(N);
+  if (tors) CUDA_TRY(cudaMemcpyAsync(rcount.data(), ctx->dec_rcount.p, sizeof(int) * tors, cudaMemcpyDeviceToHost, s));
+  if (N) {
+    CUDA_TRY(cudaMemcpyAsync(nh.data(), ctx->aux3.p, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(st.data(), ctx->dec_status.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // the staging metadata of stage(), from the counts; failed records are
+  // rejected by k_setup (pre_status) and own no right sets
+  sg.ditem_base.assign(N + 1, 0);
+  sg.right_off.assign(tors + 1, 0);
+  sg.lN.assign(N, 0);
+  sg.ln.assign(N, 0);
+  sg.lm.assign(N, 0);
+  sg.Nmax = sg.nmax = sg.mmax = 0;
+  int dbase = 0;
+  for (size_t r = 0; r < N; ++r) {
+    sg.ditem_base[r] = dbase;
+    const int Na = na[r], m = nt[r], h = st[r] == VS_REC_OK ? nh[r] : 0;
+    sg.lN[r] = Na;
+    sg.ln[r] = h;
+    sg.lm[r] = m;
+    if (st[r] == VS_REC_OK && Na <= VS_MAX_ATOMS && m <= VS_MAX_TORSIONS && h <= VS_MAX_HEAVY) {
+      sg.Nmax = std::max(sg.Nmax, Na);
+      sg.mmax = std::max(sg.mmax, m);
+      sg.nmax = std::max(sg.nmax, h);
+    }
+    dbase += std::min(m, VS_MAX_TORSIONS) * std::min(Na, VS_MAX_ATOMS);
+    for (int q = 0; q < m; ++q) {
+      const size_t t = static_cast<size_t>(sg.tors_off[r]) + q;
+      sg.right_off[t + 1] = sg.right_off[t] + (st[r] == VS_REC_OK ? rcount[t] : 0);
+      if (st[r] != VS_REC_OK) rcount[t] = 0;
+    }
+  }
+  sg.ditem_base[N] = dbase;
+  if ((rc = h2d(ctx->ditem_base, sg.ditem_base.data(), N + 1, s))) return rc;
+  if ((rc = h2d(ctx->right_off, sg.right_off.data(), tors + 1, s))) return rc;
+  if ((rc = h2d(ctx->dec_rcount, rcount.data(), tors, s))) return rc;
+  std::vector<int32_t> pre(N);
+  for (size_t r = 0; r < N; ++r) pre[r] = st[r] != VS_REC_OK;
+  if ((rc = h2d(ctx->aux2, pre.data(), N, s))) return rc;
+  CUDA_TRY(ctx->right_atoms.ensure(sizeof(uint16_t) * std::max<int>(sg.right_off[tors], 1)));
+  CUDA_TRY(vsd::launch_compact_right(ctx->dec_rslots.as<uint16_t>(), ctx->dec_rsoff.as<int64_t>(),
+                                     ctx->dec_rcount.as<int>(), ctx->right_off.as<int>(), static_cast<int>(tors),
+                                     ctx->right_atoms.as<uint16_t>(), s));
+  const size_t ta = std::max<size_t>(atoms, 1), tt = std::max<size_t>(tors, 1);
+  CUDA_TRY(ctx->meta.ensure(sizeof(vsd::lig_meta) * std::max<size_t>(N, 1)));
+  CUDA_TRY(ctx->tmask.ensure(4 * ta));
+  CUDA_TRY(ctx->heavy_list.ensure(2 * ta));
+  CUDA_TRY(ctx->dmask.ensure(4 * ta));
+  CUDA_TRY(ctx->tors_a.ensure(2 * tt));
+  CUDA_TRY(ctx->tors_b.ensure(2 * tt));
+  CUDA_TRY(ctx->d_count.ensure(4 * tt));
+  CUDA_TRY(ctx->d_off.ensure(4 * tt));
+  CUDA_TRY(ctx->ditems.ensure(2 * static_cast<size_t>(std::max(dbase, 1))));
+  CUDA_TRY(ctx->titems.ensure(8 * static_cast<size_t>(std::max(dbase, 1))));
+  vsd::batch_dev &b = sg.b;
+  b.n_lig = n;
+  b.pre_status = ctx->aux2.as<int>();
+  b.atom_off = ctx->atom_off.as<int>();
+  b.bond_off = ctx->bond_off.as<int>();
+  b.tors_off = ctx->tors_off.as<int>();
+  b.ditem_base = ctx->ditem_base.as<int>();
+  b.xyz = ctx->xyz.as<double>();
+  b.elem = ctx->elem.as<uint8_t>();
+  b.heavy = ctx->heavy.as<uint8_t>();
+  b.bond_a = ctx->bond_a.as<uint16_t>();
+  b.bond_b = ctx->bond_b.as<uint16_t>();
+  b.tors_bond = ctx->tors_bond.as<uint16_t>();
+  b.right_off = ctx->right_off.as<int>();
+  b.right_atoms = ctx->right_atoms.as<uint16_t>();
+  b.meta = ctx->meta.as<vsd::lig_meta>();
+  b.atom_tmask = ctx->tmask.as<uint32_t>();
+  b.heavy_list = ctx->heavy_list.as<uint16_t>();
+  b.heavy_dmask = ctx->dmask.as<uint32_t>();
+  b.tors_a = ctx->tors_a.as<uint16_t>();
+  b.tors_b = ctx->tors_b.as<uint16_t>();
+  b.d_count = ctx->d_count.as<int>();
+  b.d_off = ctx->d_off.as<int>();
+  b.ditems = ctx->ditems.as<uint16_t>();
+  b.titems = ctx->titems.as<uint32_t>();
+  if (record_status)
+    for (size_t r = 0; r < N; ++r) record_status[r] = st[r];
+  std::vector<vs_dock_result *> res(static_cast<size_t>(n_pockets));
+  for (int p = 0; p < n_pockets; ++p) res[p] = results + static_cast<size_t>(p) * N;
+  return dock_impl(ctx, pockets, n_pockets, nullptr, cfg, res.data(), nullptr, nullptr, nullptr, &sg);
 }

@@ -47,6 +47,11 @@ __global__ void k_setup(batch_dev b, int restarts) {
   const int b0 = b.bond_off[l], nb = b.bond_off[l + 1] - b0;
   const int t0 = b.tors_off[l], m = b.tors_off[l + 1] - t0;
   lig_meta meta{N, 0, m, VS_LIG_OK, 0, 0, 0};
+  if (b.pre_status && b.pre_status[l] != 0) {  // a record that failed to decode (vs_dock_records)
+    meta.status = VS_LIG_BAD_RECORD;
+    b.meta[l] = meta;
+    return;
+  }
   // apply_torsion's index checks (transform.cpp:56-57, 66-67) fire in the
   // first flatten pass, before any coordinate is used.
   if (m > VS_MAX_TORSIONS) meta.status = VS_LIG_TOO_LARGE;

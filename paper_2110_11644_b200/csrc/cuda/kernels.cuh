@@ -24,6 +24,7 @@ struct lig_meta {
 // Device copy of one batch (vs_ligand_batch) plus derived arrays.
 struct batch_dev {
   int n_lig;
+  const int *pre_status;   // n or NULL: nonzero = reject the ligand (records that failed to decode)
   const int *atom_off;     // n+1
   const int *bond_off;     // n+1
   const int *tors_off;     // n+1
@@ -119,7 +120,9 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
 cudaError_t launch_decode(const uint8_t *bytes, const int64_t *offs, int n, const int *atom_off, const int *bond_off,
                           const int *tors_off, const int64_t *rs_off, double *xyz, uint8_t *elem, uint8_t *heavy,
                           uint8_t *border, uint16_t *ba, uint16_t *bb, uint16_t *tbond, uint16_t *rslots, int *rcount,
-                          int *status, cudaStream_t s);
+                          int *status, cudaStream_t s, int *nheavy = nullptr);
+cudaError_t launch_compact_right(const uint16_t *slots, const int64_t *rs_off, const int *rcount, const int *right_off,
+                                 int n_tors, uint16_t *right_atoms, cudaStream_t s);
 size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms);
 // dynamic shared memory of one k_search CTA for the given ligand maxima
 size_t search_smem_bytes(int N, int n, int m, int dtot);

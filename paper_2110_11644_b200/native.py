@@ -65,6 +65,8 @@ SIGNATURES = {
     "vs_decode_records": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.c_int64, C.POINTER(C.c_int64), C.c_int32,
                                     C.POINTER(_vp)]),
     "vs_encode_records": (C.c_int64, [_LB, C.POINTER(C.c_char_p), C.c_void_p, C.c_int64]),
+    "vs_dock_records": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, C.POINTER(C.c_uint8), C.c_int64,
+                                  C.POINTER(C.c_int64), C.c_int32, _CF, _DR, C.POINTER(C.c_int32)]),
     "vs_ligand_set_free": (None, [_vp]),
     "vs_detect_torsions": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint8)]),
     "vs_bridge_bonds": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint8)]),

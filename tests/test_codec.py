@@ -137,3 +137,28 @@ def test_gpu_decode_disconnected_and_framing(gpu_ctx, ref):
     _, status, _ = api.decode_records(a[:-3], [0], gpu_ctx)
     assert status[0] == 2
     assert list(api.frame_records(a + b[:-1])) == [0]
+
+
+@pytest.mark.gpu
+def test_gpu_dock_records_equals_decode_then_dock(gpu_ctx, ref):
+    """vs_dock_records (decode into the dock path's device inputs) gives the
+    results of decode_records + dock_and_score_batch, record for record; a
+    corrupt record in the stream only fails itself."""
+    from paper_2110_11644_b200 import abi, synth
+    el, xyz = synth.synthetic_protein()
+    pocket = api.build_pocket(el, xyz, [0.0, 0.0, 0.0], 12.0, 0.375, gpu_ctx)
+    smi = api.synthetic_smiles(40, seed=5)
+    ligs = api.prepare_ligand(smi, quantize=True, ctx=gpu_ctx)
+    data = bytearray(api.encode_records(ligs))
+    offs = list(api.frame_records(bytes(data)))
+    bad = 7  # an invalid element code in record 7
+    name_len = struct.unpack_from("<H", data, offs[bad] + 6)[0]
+    data[offs[bad] + 8 + name_len + 6 + 12] = 77
+    data = bytes(data)
+    cfg = abi.ScoringConfig(restarts=6, rescored=4)
+    res, rst, _, _ = api.dock_records([pocket], data, offs, cfg, gpu_ctx)
+    assert rst[bad] == 4 and res[0][bad]["status"] == abi.VS_LIG_BAD_RECORD
+    dec, status, _ = api.decode_records(data, offs, gpu_ctx)
+    good = [i for i in range(len(offs)) if i != bad]
+    want = api.dock_and_score_batch(pocket, [dec[i] for i in good], cfg, gpu_ctx, want_conformation=False).results
+    assert np.array_equal(res[0][good].view(np.uint8), want.view(np.uint8))
