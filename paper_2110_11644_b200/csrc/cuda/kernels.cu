@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
   }
   __syncthreads();
   for (int sweep = 0; sweep < max_sweeps && m > 0; ++sweep) {
+    __syncthreads();  // every thread has read the previous sweep's `changed`
     if (tid == 0) sweeps_done = sweep + 1;
     for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
     if (tid == 0) changed = 0;
@@ -312,11 +313,367 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
   if (tid == 0) f.sweeps[l] = sweeps_done;
 }
 
+// ============================================================== k_flatten_dep
+// The same flatten, organised around what the 36 candidates of torsion t
+// actually change.  The spread sums only feed an argmax (search.cpp:52-58), so
+// a candidate needs its exact sequential sum (transform.cpp:83-90) only when
+// another candidate comes within rounding distance of it:
+//   * D_t = atoms whose final position depends on the candidate: moved by t or
+//     by a later torsion whose axis moves with the candidate (closure over
+//     u > t).  Every other atom ends where all candidates put it; that common
+//     position (Q) and the matrices of the candidate-independent torsions are
+//     computed once per t by warp 0 -- the same operations on the same values
+//     as in every candidate of the legacy kernel, so bit-identical.
+//   * 8 lanes per candidate (288 threads = 36 x 8, no idle lane) transform the
+//     D_t atoms and sum the distances of the pairs that touch D_t, in any
+//     order ("A_o"); pairs of two common atoms add the same I to every
+//     candidate and are only bounded (I <= (n_I - 1) * sum |q - q_0|).
+//   * The reference's choice is the first argmax of R_o = fl_seq(I + T_o).
+//     With n pairs, |R_o - (I + T_o)| <= gamma_n (I + T_o) and our A_o carries
+//     at most the same plus the 2^-50 of the filter square root, so
+//     A_best - A_o > (2 I_bound + A_best + A_o) * n * 2^-49 proves
+//     R_best > R_o.  Candidates that fail the test (near ties: symmetric
+//     groups, ~2% of decisions) get the exact sequential sum of the legacy
+//     kernel, and the argmax is taken over those exact values.
+// The decision, and so every output, is bit-identical to the legacy kernel.
+constexpr int kFC = 36;         // candidates per torsion (10-degree lattice offsets)
+constexpr int kFL = 8;          // lanes per candidate
+constexpr int kFT = kFC * kFL;  // 288 threads = 9 full warps
+
+// sqrt for the filter sums: MUFU seed + one third-order step, relative error
+// below 2^-50 (no final rounding correction; the bound above allows for it).
+__device__ __forceinline__ double dsqrt_filter(double x) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  const double e = fma(x, -(y0 * y0), 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  const double y1 = fma(p, y0 * e, y0);
+  return x < 0x1p-1000 ? 0.0 : x * y1;
+}
+
+size_t flatten_dep_smem(int nmax, int mmax) {
+  return (size_t)(3 * nmax + 3 * nmax + 4 * nmax + 3 * nmax * kFC + 18 * mmax + 2 * kFC + 12) * sizeof(double) +
+         (size_t)4 * nmax * sizeof(int);
+}
+
+#ifndef VS_FLAT_MINB
+#define VS_FLAT_MINB 3
+#endif
+__global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, int max_sweeps, flat_out f, int nmax, int mmax,
+                                                     const int *lig_index) {
+  extern __shared__ double sm[];
+  const int l = lig_index ? lig_index[blockIdx.x] : blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const lig_meta meta = b.meta[l];
+  const int a0 = b.atom_off[l], t0 = b.tors_off[l];
+  const int N = meta.n_atoms, m = meta.m;
+  if (meta.status != VS_LIG_OK) return;
+  double *P = sm;                       // [N][3] stage-t prefix (torsions < t applied)
+  double *Q = P + 3 * nmax;             // [N][3] common positions (candidate-independent torsions applied)
+  double *Qc = Q + 3 * nmax;            // [n_I][4] Q of the common atoms, compacted
+  double *C = Qc + 4 * nmax;            // [rank][xyz][36] candidate positions of the D_t atoms
+  double *Ms = C + 3 * nmax * kFC;      // [u][12] matrices of the candidate-independent torsions
+  double *AX = Ms + 12 * mmax;          // [u][6] stage-u axis endpoints of the dependent torsions
+  double *spread = AX + 6 * mmax;       // [36] filter sums A_o
+  double *exact = spread + kFC;         // [36] exact sequential sums (near ties only)
+  double *mat = exact + kFC;            // [12] prefix advance
+  int *dl = reinterpret_cast<int *>(mat + 12);  // rank -> atom
+  int *nl = dl + nmax;                          // common atoms, ascending
+  int *slot = nl + nmax;                        // atom -> rank, -1 for common atoms
+  uint32_t *tmr = reinterpret_cast<uint32_t *>(slot + nmax);  // right-set mask of rank r
+  __shared__ int idx[VS_MAX_TORSIONS + 1];
+  __shared__ int changed, bad, sweeps_done, s_nd, s_nn;
+  __shared__ uint32_t s_dt, s_du;
+  __shared__ double s_ib;
+  __shared__ unsigned long long s_w;
+  const double *base = b.xyz + 3 * (size_t)a0;
+  const uint32_t *tm = b.atom_tmask + a0;
+  const int b0 = b.bond_off[l];
+  const int o = tid >> 3, g = tid & 7;
+  double *Co = C + o;  // element (r, c) of this lane's candidate at Co[(3r + c) * kFC]
+  const double npairs = 0.5 * (double)N * (double)(N - 1);
+  if (tid < m) idx[tid] = 0;
+  if (tid == 0) {
+    bad = 0;
+    sweeps_done = 0;
+  }
+  __syncthreads();
+  for (int sweep = 0; sweep < max_sweeps && m > 0; ++sweep) {
+    __syncthreads();  // every thread has read the previous sweep's `changed`
+    if (tid == 0) sweeps_done = sweep + 1;
+    for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int t = 0; t < m; ++t) {
+      // ---- A (warp 0): D_t, the common positions, the shared matrices
+      if (tid < 32) {
+        uint32_t dt = 1u << t;
+        for (int u = t + 1; u < m; ++u) {
+          const int bi = b.tors_bond[t0 + u];
+          if ((tm[b.bond_a[b0 + bi]] | tm[b.bond_b[b0 + bi]]) & dt) dt |= 1u << u;
+        }
+        int nd = 0, nn = 0;
+        uint32_t du = 0;
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          const int a = c0 + lane;
+          const uint32_t ma = a < N ? tm[a] : 0u;
+          const bool in = a < N;
+          const bool dep = in && (ma & dt);
+          const unsigned bd = __ballot_sync(0xffffffffu, dep), bn = __ballot_sync(0xffffffffu, in && !dep);
+          const unsigned below = (1u << lane) - 1u;
+          if (dep) {
+            const int r = nd + __popc(bd & below);
+            dl[r] = a;
+            slot[a] = r;
+            tmr[r] = ma;
+            du |= ma;
+          } else if (in) {
+            nl[nn + __popc(bn & below)] = a;
+            slot[a] = -1;
+          }
+          nd += __popc(bd);
+          nn += __popc(bn);
+        }
+        du = __reduce_or_sync(0xffffffffu, du);
+        for (int i = lane; i < 3 * N; i += 32) Q[i] = P[i];
+        __syncwarp();
+        for (int u = t + 1; u < m; ++u) {
+          const int bi = b.tors_bond[t0 + u];
+          const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+          if ((dt >> u) & 1u) {
+            if (lane < 3) {
+              AX[6 * u + lane] = Q[3 * ea + lane];
+              AX[6 * u + 3 + lane] = Q[3 * eb + lane];
+            }
+          } else {
+            double M[12], s, c;
+            lattice_sc(idx[u], s, c);
+            if (!torsion_setup(ld3(Q + 3 * ea), ld3(Q + 3 * eb), s, c, M) && lane == 0) bad = 1;
+            if (lane == 0)
+#pragma unroll
+              for (int k = 0; k < 12; ++k) Ms[12 * u + k] = M[k];
+            __syncwarp();  // everyone has read the endpoints
+            for (int a = lane; a < N; a += 32)
+              if ((tm[a] >> u) & 1u) st3(Q + 3 * a, torsion_apply(M, ld3(Q + 3 * a)));
+          }
+          __syncwarp();
+        }
+        // compacted common positions and the bound on their pair sum
+        double acc = 0.0;
+        const d3 q0 = nn > 0 ? ld3(Q + 3 * nl[0]) : d3{0.0, 0.0, 0.0};
+        for (int k = lane; k < nn; k += 32) {
+          const d3 q = ld3(Q + 3 * nl[k]);
+          Qc[4 * k] = q.x;
+          Qc[4 * k + 1] = q.y;
+          Qc[4 * k + 2] = q.z;
+          acc += dsqrt_filter(sqn3(sub3(q, q0)));
+        }
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+        if (lane == 0) {
+          s_nd = nd;
+          s_nn = nn;
+          s_dt = dt;
+          s_du = du;
+          s_ib = acc * (double)(nn > 0 ? nn - 1 : 0) * (1.0 + 0x1p-40);
+        }
+      }
+      __syncthreads();
+      // ---- B: this lane's share of its candidate's D_t atoms through t..m-1
+      const int nd = s_nd, nn = s_nn;
+      const uint32_t dt = s_dt, du = s_du;
+      for (int r = g; r < nd; r += kFL) {
+        const int a = dl[r];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Co[(3 * r + c) * kFC] = P[3 * a + c];
+      }
+      __syncwarp();
+      for (int u = t; u < m; ++u) {
+        if (!(((du | dt) >> u) & 1u)) continue;  // candidate-independent and moves no D_t atom
+        double M[12];
+        if ((dt >> u) & 1u) {
+          const int bi = b.tors_bond[t0 + u];
+          const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+          d3 pa, pb;
+          if (u == t) {
+            pa = ld3(P + 3 * ea);
+            pb = ld3(P + 3 * eb);
+          } else {
+            const int sa = slot[ea], sb = slot[eb];
+            pa = sa >= 0 ? d3{Co[(3 * sa) * kFC], Co[(3 * sa + 1) * kFC], Co[(3 * sa + 2) * kFC]} : ld3(AX + 6 * u);
+            pb = sb >= 0 ? d3{Co[(3 * sb) * kFC], Co[(3 * sb + 1) * kFC], Co[(3 * sb + 2) * kFC]}
+                         : ld3(AX + 6 * u + 3);
+          }
+          double s, c;
+          lattice_sc(u == t ? (idx[t] + o) % 36 : idx[u], s, c);
+          if (!torsion_setup(pa, pb, s, c, M)) bad = 1;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 12; ++k) M[k] = Ms[12 * u + k];
+        }
+        __syncwarp();  // endpoints read before anyone moves them
+        for (int r = g; r < nd; r += kFL)
+          if ((tmr[r] >> u) & 1u) {
+            double *x = Co + 3 * r * kFC;
+            const d3 y = torsion_apply(M, d3{x[0], x[kFC], x[2 * kFC]});
+            x[0] = y.x;
+            x[kFC] = y.y;
+            x[2 * kFC] = y.z;
+          }
+        __syncwarp();
+      }
+      // ---- C: filter sum over the pairs that touch D_t.  Row r (rank) pairs
+      // with every common atom, then with the ranks after r; the lanes of a
+      // candidate stride the flattened pair list by 8.
+      {
+        double acc = 0.0;
+        int r = 0, k = g, len = nn + nd - 1;
+        while (r < nd && k >= len) {
+          k -= len;
+          ++r;
+          len = nn + nd - 1 - r;
+        }
+        d3 xi{0.0, 0.0, 0.0};
+        if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+        while (r < nd) {
+          const bool cross = k < nn;
+          const double *pp = cross ? Qc + 4 * k : Co + 3 * (r + 1 + k - nn) * kFC;
+          const int st = cross ? 1 : kFC;
+          const d3 xj{pp[0], pp[st], pp[2 * st]};
+          acc += dsqrt_filter(sqn3(sub3(xi, xj)));
+          k += kFL;
+          if (k >= len) {
+            do {
+              k -= len;
+              ++r;
+              len = nn + nd - 1 - r;
+            } while (r < nd && k >= len);
+            if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+          }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        if (g == 0) spread[o] = acc;
+      }
+      __syncthreads();
+      // ---- D: certain winner, or the set of candidates within rounding of it
+      if (tid == 0) {
+        int bo = 0;
+        double bv = -__longlong_as_double(0x7ff0000000000000LL);
+        for (int q = 0; q < kFC; ++q)
+          if (spread[q] > bv) {
+            bv = spread[q];
+            bo = q;
+          }
+        unsigned long long w = 1ull << bo;
+        const double ib2 = 2.0 * s_ib;
+        for (int q = 0; q < kFC; ++q) {
+          const double mg = (ib2 + bv + spread[q]) * npairs * 0x1p-49 + 0x1p-900;
+          if (q != bo && !(bv - spread[q] > mg)) w |= 1ull << q;
+        }
+#ifdef VS_FLAT_FORCE_EXACT
+        w = (1ull << kFC) - 1;
+#endif
+        s_w = w;
+      }
+      __syncthreads();
+      const unsigned long long w = s_w;
+      if (__popcll(w) > 1) {
+        // exact sequential sums (transform.cpp:83-90) of the near-tied candidates
+        if (tid < kFC && ((w >> tid) & 1ull)) {
+          const double *Ct = C + tid;
+          double sum = 0.0;
+          for (int i = 0; i + 1 < N; ++i) {
+            const int si = slot[i];
+            const d3 xi = si >= 0 ? d3{Ct[(3 * si) * kFC], Ct[(3 * si + 1) * kFC], Ct[(3 * si + 2) * kFC]}
+                                  : ld3(Q + 3 * i);
+            for (int j = i + 1; j < N; ++j) {
+              const int sj = slot[j];
+              const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
+                                    : ld3(Q + 3 * j);
+              sum += dsqrt_dist2(sqn3(sub3(xi, xj)));
+            }
+          }
+          exact[tid] = sum;
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        int best_off = 0;
+        if (__popcll(w) > 1) {
+          double best = -__longlong_as_double(0x7ff0000000000000LL);
+          for (int q = 0; q < kFC; ++q)
+            if (((w >> q) & 1ull) && exact[q] > best) {
+              best = exact[q];
+              best_off = q;
+            }
+        } else {
+          best_off = __ffsll(w) - 1;
+        }
+        if (best_off != 0) {
+          idx[t] = (idx[t] + best_off) % 36;
+          changed = 1;
+        }
+        const int bi = b.tors_bond[t0 + t];
+        const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+        double s, c;
+        lattice_sc(idx[t], s, c);
+        if (!torsion_setup(ld3(P + 3 * ea), ld3(P + 3 * eb), s, c, mat)) bad = 1;
+      }
+      __syncthreads();
+      if (bad) break;
+      for (int a = tid; a < N; a += blockDim.x)
+        if ((tm[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(mat, ld3(P + 3 * a)));
+      __syncthreads();
+    }
+    if (bad || !changed) break;
+  }
+  if (bad) {
+    if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
+    return;
+  }
+  for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
+  __syncthreads();
+  for (int t = 0; t < m; ++t) {
+    if (tid == 0) {
+      const int bi = b.tors_bond[t0 + t];
+      const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+      double s, c;
+      lattice_sc(idx[t], s, c);
+      if (!torsion_setup(ld3(P + 3 * ea), ld3(P + 3 * eb), s, c, mat)) bad = 1;
+    }
+    __syncthreads();
+    if (bad) break;
+    for (int a = tid; a < N; a += blockDim.x)
+      if ((tm[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(mat, ld3(P + 3 * a)));
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
+    return;
+  }
+  for (int i = tid; i < 3 * N; i += blockDim.x) f.xyz[3 * (size_t)a0 + i] = P[i];
+  if (tid < m) f.idx[t0 + tid] = idx[tid];
+  if (tid < 3) f.centroid[3 * l + tid] = centroid_row(P, N, tid);
+  if (tid == 0) f.sweeps[l] = sweeps_done;
+}
+
+#ifndef VS_FLAT_LEGACY
+#define VS_FLAT_LEGACY 0
+#endif
+
 cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f, int nmax_atoms, int mmax,
                            cudaStream_t s, const int *lig_index, int n_lig) {
   const int n = lig_index ? n_lig : b.n_lig;
   if (n == 0) return cudaSuccess;
-  (void)mmax;
+  const int mm = mmax < 1 ? 1 : mmax;
+  const size_t dsmem = flatten_dep_smem(nmax_atoms, mm);
+  if (!VS_FLAT_LEGACY && dsmem <= 200 * 1024) {
+    cudaFuncSetAttribute(k_flatten_dep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+    k_flatten_dep<<<n, kFT, dsmem, s>>>(b, max_sweeps, f, nmax_atoms, mm, lig_index);
+    return cudaGetLastError();
+  }
   int cb = 36;
   auto bytes = [&](int c) { return (size_t)(3 * nmax_atoms * (1 + c) + 36 + 12) * sizeof(double); };
   while (cb > 1 && bytes(cb) > 200 * 1024) cb = (cb + 1) / 2;
