@@ -352,15 +352,15 @@ __device__ __forceinline__ double dsqrt_filter(double x) {
 }
 
 size_t flatten_dep_smem(int nmax, int mmax) {
-  return (size_t)(3 * nmax + 3 * nmax + 4 * nmax + 3 * nmax * kFC + 18 * mmax + 2 * kFC + 12) * sizeof(double) +
-         (size_t)4 * nmax * sizeof(int);
+  return (size_t)(3 * nmax + 3 * nmax + 4 * nmax + 3 * nmax * kFC + 18 * mmax + kFC) * sizeof(double) +
+         (size_t)(5 * nmax + mmax) * sizeof(int);
 }
 
 #ifndef VS_FLAT_MINB
 #define VS_FLAT_MINB 3
 #endif
-__global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, int max_sweeps, flat_out f, int nmax, int mmax,
-                                                     const int *lig_index) {
+__global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, int max_sweeps, flat_out f, int nmax,
+                                                                   int mmax, const int *lig_index) {
   extern __shared__ double sm[];
   const int l = lig_index ? lig_index[blockIdx.x] : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -368,56 +368,61 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   const int a0 = b.atom_off[l], t0 = b.tors_off[l];
   const int N = meta.n_atoms, m = meta.m;
   if (meta.status != VS_LIG_OK) return;
-  double *P = sm;                       // [N][3] stage-t prefix (torsions < t applied)
-  double *Q = P + 3 * nmax;             // [N][3] common positions (candidate-independent torsions applied)
-  double *Qc = Q + 3 * nmax;            // [n_I][4] Q of the common atoms, compacted
-  double *C = Qc + 4 * nmax;            // [rank][xyz][36] candidate positions of the D_t atoms
-  double *Ms = C + 3 * nmax * kFC;      // [u][12] matrices of the candidate-independent torsions
-  double *AX = Ms + 12 * mmax;          // [u][6] stage-u axis endpoints of the dependent torsions
-  double *spread = AX + 6 * mmax;       // [36] filter sums A_o
-  double *exact = spread + kFC;         // [36] exact sequential sums (near ties only)
-  double *mat = exact + kFC;            // [12] prefix advance
-  int *dl = reinterpret_cast<int *>(mat + 12);  // rank -> atom
-  int *nl = dl + nmax;                          // common atoms, ascending
-  int *slot = nl + nmax;                        // atom -> rank, -1 for common atoms
-  uint32_t *tmr = reinterpret_cast<uint32_t *>(slot + nmax);  // right-set mask of rank r
+  double *P = sm;                   // [N][3] stage-t prefix (torsions < t applied)
+  double *Q = P + 3 * nmax;         // [N][3] common positions (candidate-independent torsions applied)
+  double *Qc = Q + 3 * nmax;        // [n_I][4] Q of the common atoms, compacted
+  double *C = Qc + 4 * nmax;        // [rank][xyz][36] candidate positions of the D_t atoms
+  double *Ms = C + 3 * nmax * kFC;  // [u][12] matrices of the candidate-independent torsions
+  double *AX = Ms + 12 * mmax;      // [u][6] stage-u axis endpoints of the dependent torsions
+  double *spread = AX + 6 * mmax;   // [36] filter sums A_o
+  int *dl = reinterpret_cast<int *>(spread + kFC);            // rank -> atom
+  int *nl = dl + nmax;                                        // common atoms, ascending
+  int *slot = nl + nmax;                                      // atom -> rank, -1 for common atoms
+  uint32_t *tms = reinterpret_cast<uint32_t *>(slot + nmax);  // right-set masks of the atoms
+  uint32_t *tmr = tms + nmax;                                 // right-set mask of rank r
+  int *tax = reinterpret_cast<int *>(tmr + nmax);             // torsion u's axis atoms, ea | eb << 16
   __shared__ int idx[VS_MAX_TORSIONS + 1];
   __shared__ int changed, bad, sweeps_done, s_nd, s_nn;
   __shared__ uint32_t s_dt, s_du;
   __shared__ double s_ib;
-  __shared__ unsigned long long s_w;
   const double *base = b.xyz + 3 * (size_t)a0;
-  const uint32_t *tm = b.atom_tmask + a0;
-  const int b0 = b.bond_off[l];
   const int o = tid >> 3, g = tid & 7;
   double *Co = C + o;  // element (r, c) of this lane's candidate at Co[(3r + c) * kFC]
   const double npairs = 0.5 * (double)N * (double)(N - 1);
-  if (tid < m) idx[tid] = 0;
+  const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
+  if (tid < m) {
+    idx[tid] = 0;
+    const int bi = b.tors_bond[t0 + tid], b0 = b.bond_off[l];
+    tax[tid] = b.bond_a[b0 + bi] | (b.bond_b[b0 + bi] << 16);
+  }
+  for (int a = tid; a < N; a += blockDim.x) tms[a] = b.atom_tmask[a0 + a];
   if (tid == 0) {
     bad = 0;
     sweeps_done = 0;
   }
   __syncthreads();
   for (int sweep = 0; sweep < max_sweeps && m > 0; ++sweep) {
-    __syncthreads();  // every thread has read the previous sweep's `changed`
-    if (tid == 0) sweeps_done = sweep + 1;
+    if (sweep) __syncthreads();  // every thread has read the previous sweep's `changed`
+    if (tid == 0) {
+      sweeps_done = sweep + 1;
+      changed = 0;
+    }
     for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
-    if (tid == 0) changed = 0;
     __syncthreads();
     for (int t = 0; t < m; ++t) {
       // ---- A (warp 0): D_t, the common positions, the shared matrices
       if (tid < 32) {
         uint32_t dt = 1u << t;
         for (int u = t + 1; u < m; ++u) {
-          const int bi = b.tors_bond[t0 + u];
-          if ((tm[b.bond_a[b0 + bi]] | tm[b.bond_b[b0 + bi]]) & dt) dt |= 1u << u;
+          const int ax = tax[u];
+          if ((tms[ax & 0xffff] | tms[ax >> 16]) & dt) dt |= 1u << u;
         }
         int nd = 0, nn = 0;
         uint32_t du = 0;
         for (int c0 = 0; c0 < N; c0 += 32) {
           const int a = c0 + lane;
-          const uint32_t ma = a < N ? tm[a] : 0u;
           const bool in = a < N;
+          const uint32_t ma = in ? tms[a] : 0u;
           const bool dep = in && (ma & dt);
           const unsigned bd = __ballot_sync(0xffffffffu, dep), bn = __ballot_sync(0xffffffffu, in && !dep);
           const unsigned below = (1u << lane) - 1u;
@@ -438,8 +443,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         for (int i = lane; i < 3 * N; i += 32) Q[i] = P[i];
         __syncwarp();
         for (int u = t + 1; u < m; ++u) {
-          const int bi = b.tors_bond[t0 + u];
-          const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+          const int ax = tax[u], ea = ax & 0xffff, eb = ax >> 16;
           if ((dt >> u) & 1u) {
             if (lane < 3) {
               AX[6 * u + lane] = Q[3 * ea + lane];
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
               for (int k = 0; k < 12; ++k) Ms[12 * u + k] = M[k];
             __syncwarp();  // everyone has read the endpoints
             for (int a = lane; a < N; a += 32)
-              if ((tm[a] >> u) & 1u) st3(Q + 3 * a, torsion_apply(M, ld3(Q + 3 * a)));
+              if ((tms[a] >> u) & 1u) st3(Q + 3 * a, torsion_apply(M, ld3(Q + 3 * a)));
           }
           __syncwarp();
         }
@@ -479,6 +483,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         }
       }
       __syncthreads();
+      if (bad) break;
       // ---- B: this lane's share of its candidate's D_t atoms through t..m-1
       const int nd = s_nd, nn = s_nn;
       const uint32_t dt = s_dt, du = s_du;
@@ -492,8 +497,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         if (!(((du | dt) >> u) & 1u)) continue;  // candidate-independent and moves no D_t atom
         double M[12];
         if ((dt >> u) & 1u) {
-          const int bi = b.tors_bond[t0 + u];
-          const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
+          const int ax = tax[u], ea = ax & 0xffff, eb = ax >> 16;
           d3 pa, pb;
           if (u == t) {
             pa = ld3(P + 3 * ea);
@@ -522,33 +526,49 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           }
         __syncwarp();
       }
-      // ---- C: filter sum over the pairs that touch D_t.  Row r (rank) pairs
-      // with every common atom, then with the ranks after r; the lanes of a
-      // candidate stride the flattened pair list by 8.
+      // ---- C: filter sum over the pairs that touch D_t, in two flattened
+      // walks strided by the 8 lanes of the candidate: (rank r, common k),
+      // then (rank r, rank s > r).
       {
         double acc = 0.0;
-        int r = 0, k = g, len = nn + nd - 1;
-        while (r < nd && k >= len) {
-          k -= len;
-          ++r;
-          len = nn + nd - 1 - r;
+        if (nn > 0) {
+          int r = g / nn, k = g - r * nn;
+          d3 xi{0.0, 0.0, 0.0};
+          if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+          while (r < nd) {
+            const double *q = Qc + 4 * k;
+            acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[1], q[2]})));
+            k += kFL;
+            if (k >= nn) {
+              do {
+                k -= nn;
+                ++r;
+              } while (k >= nn);
+              if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+            }
+          }
         }
-        d3 xi{0.0, 0.0, 0.0};
-        if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
-        while (r < nd) {
-          const bool cross = k < nn;
-          const double *pp = cross ? Qc + 4 * k : Co + 3 * (r + 1 + k - nn) * kFC;
-          const int st = cross ? 1 : kFC;
-          const d3 xj{pp[0], pp[st], pp[2 * st]};
-          acc += dsqrt_filter(sqn3(sub3(xi, xj)));
-          k += kFL;
-          if (k >= len) {
-            do {
-              k -= len;
-              ++r;
-              len = nn + nd - 1 - r;
-            } while (r < nd && k >= len);
-            if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+        {
+          int r = 0, k = g, len = nd - 1;
+          while (r < nd - 1 && k >= len) {
+            k -= len;
+            ++r;
+            len = nd - 1 - r;
+          }
+          d3 xi{0.0, 0.0, 0.0};
+          if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+          while (r < nd - 1) {
+            const double *q = Co + 3 * (r + 1 + k) * kFC;
+            acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
+            k += kFL;
+            if (k >= len) {
+              do {
+                k -= len;
+                ++r;
+                len = nd - 1 - r;
+              } while (r < nd - 1 && k >= len);
+              if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+            }
           }
         }
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -557,98 +577,113 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         if (g == 0) spread[o] = acc;
       }
       __syncthreads();
-      // ---- D: certain winner, or the set of candidates within rounding of it
-      if (tid == 0) {
-        int bo = 0;
-        double bv = -__longlong_as_double(0x7ff0000000000000LL);
-        for (int q = 0; q < kFC; ++q)
-          if (spread[q] > bv) {
-            bv = spread[q];
-            bo = q;
-          }
-        unsigned long long w = 1ull << bo;
-        const double ib2 = 2.0 * s_ib;
-        for (int q = 0; q < kFC; ++q) {
-          const double mg = (ib2 + bv + spread[q]) * npairs * 0x1p-49 + 0x1p-900;
-          if (q != bo && !(bv - spread[q] > mg)) w |= 1ull << q;
+      // ---- D (warp 0): certain winner, or the exact sums of the candidates
+      // within rounding of it; then the prefix advance (search.cpp:52-60)
+      if (tid < 32) {
+        // first argmax (the reference's strict > from -inf; NaN never wins)
+        const double v0 = spread[lane], v1 = lane + 32 < kFC ? spread[lane + 32] : ninf;
+        double bv = v0 == v0 ? v0 : ninf;
+        int bo = lane;
+        if (v1 > bv) {
+          bv = v1;
+          bo = lane + 32;
         }
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, sh);
+          const int oo = __shfl_xor_sync(0xffffffffu, bo, sh);
+          if (ov > bv || (ov == bv && oo < bo)) {
+            bv = ov;
+            bo = oo;
+          }
+        }
+        if (bv == ninf) bo = 0;
+        const double ib2 = 2.0 * s_ib;
+        const bool n0 = lane != bo && !(bv - v0 > (ib2 + bv + v0) * npairs * 0x1p-49 + 0x1p-900);
+        const bool n1 = lane + 32 < kFC && lane + 32 != bo &&
+                        !(bv - v1 > (ib2 + bv + v1) * npairs * 0x1p-49 + 0x1p-900);
+        unsigned long long w = (unsigned long long)__ballot_sync(0xffffffffu, n0) |
+                               ((unsigned long long)__ballot_sync(0xffffffffu, n1) << 32);
 #ifdef VS_FLAT_FORCE_EXACT
         w = (1ull << kFC) - 1;
 #endif
-        s_w = w;
-      }
-      __syncthreads();
-      const unsigned long long w = s_w;
-      if (__popcll(w) > 1) {
-        // exact sequential sums (transform.cpp:83-90) of the near-tied candidates
-        if (tid < kFC && ((w >> tid) & 1ull)) {
-          const double *Ct = C + tid;
-          double sum = 0.0;
-          for (int i = 0; i + 1 < N; ++i) {
-            const int si = slot[i];
-            const d3 xi = si >= 0 ? d3{Ct[(3 * si) * kFC], Ct[(3 * si + 1) * kFC], Ct[(3 * si + 2) * kFC]}
-                                  : ld3(Q + 3 * i);
-            for (int j = i + 1; j < N; ++j) {
-              const int sj = slot[j];
-              const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
-                                    : ld3(Q + 3 * j);
-              sum += dsqrt_dist2(sqn3(sub3(xi, xj)));
+        w |= 1ull << bo;
+        int best_off = bo;
+        if (__popcll(w) > 1) {
+          // exact sequential sums (transform.cpp:83-90) of the near-tied
+          // candidates, first argmax among them
+          double ev = ninf;
+          int eo = lane;
+          for (int q = lane; q < kFC; q += 32) {
+            if (!((w >> q) & 1ull)) continue;
+            const double *Ct = C + q;
+            double sum = 0.0;
+            for (int i = 0; i + 1 < N; ++i) {
+              const int si = slot[i];
+              const d3 xi = si >= 0 ? d3{Ct[(3 * si) * kFC], Ct[(3 * si + 1) * kFC], Ct[(3 * si + 2) * kFC]}
+                                    : ld3(Q + 3 * i);
+              for (int j = i + 1; j < N; ++j) {
+                const int sj = slot[j];
+                const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
+                                      : ld3(Q + 3 * j);
+                sum += dsqrt_dist2(sqn3(sub3(xi, xj)));
+              }
+            }
+            if (sum > ev) {
+              ev = sum;
+              eo = q;
             }
           }
-          exact[tid] = sum;
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        int best_off = 0;
-        if (__popcll(w) > 1) {
-          double best = -__longlong_as_double(0x7ff0000000000000LL);
-          for (int q = 0; q < kFC; ++q)
-            if (((w >> q) & 1ull) && exact[q] > best) {
-              best = exact[q];
-              best_off = q;
+#pragma unroll
+          for (int sh = 16; sh; sh >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, ev, sh);
+            const int oo = __shfl_xor_sync(0xffffffffu, eo, sh);
+            if (ov > ev || (ov == ev && oo < eo)) {
+              ev = ov;
+              eo = oo;
             }
-        } else {
-          best_off = __ffsll(w) - 1;
+          }
+          best_off = ev == ninf ? 0 : eo;
         }
-        if (best_off != 0) {
-          idx[t] = (idx[t] + best_off) % 36;
+        const int nidx = (idx[t] + best_off) % 36;
+        __syncwarp();
+        if (lane == 0 && best_off != 0) {
+          idx[t] = nidx;
           changed = 1;
         }
-        const int bi = b.tors_bond[t0 + t];
-        const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
-        double s, c;
-        lattice_sc(idx[t], s, c);
-        if (!torsion_setup(ld3(P + 3 * ea), ld3(P + 3 * eb), s, c, mat)) bad = 1;
+        const int ax = tax[t];
+        double M[12], s, c;
+        lattice_sc(nidx, s, c);
+        if (!torsion_setup(ld3(P + 3 * (ax & 0xffff)), ld3(P + 3 * (ax >> 16)), s, c, M) && lane == 0) bad = 1;
+        __syncwarp();  // endpoints read before the right set moves
+        for (int a = lane; a < N; a += 32)
+          if ((tms[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(M, ld3(P + 3 * a)));
+        __syncwarp();
       }
-      __syncthreads();
-      if (bad) break;
-      for (int a = tid; a < N; a += blockDim.x)
-        if ((tm[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(mat, ld3(P + 3 * a)));
-      __syncthreads();
     }
+    __syncthreads();
     if (bad || !changed) break;
   }
   if (bad) {
     if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
     return;
   }
-  for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
-  __syncthreads();
-  for (int t = 0; t < m; ++t) {
-    if (tid == 0) {
-      const int bi = b.tors_bond[t0 + t];
-      const int ea = b.bond_a[b0 + bi], eb = b.bond_b[b0 + bi];
-      double s, c;
+  // flat conformation = apply_torsions(base, angles_of(index)) (search.cpp:67-68)
+  if (tid < 32) {
+    for (int i = lane; i < 3 * N; i += 32) P[i] = base[i];
+    __syncwarp();
+    for (int t = 0; t < m; ++t) {
+      const int ax = tax[t];
+      double M[12], s, c;
       lattice_sc(idx[t], s, c);
-      if (!torsion_setup(ld3(P + 3 * ea), ld3(P + 3 * eb), s, c, mat)) bad = 1;
+      if (!torsion_setup(ld3(P + 3 * (ax & 0xffff)), ld3(P + 3 * (ax >> 16)), s, c, M) && lane == 0) bad = 1;
+      __syncwarp();
+      for (int a = lane; a < N; a += 32)
+        if ((tms[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(M, ld3(P + 3 * a)));
+      __syncwarp();
     }
-    __syncthreads();
-    if (bad) break;
-    for (int a = tid; a < N; a += blockDim.x)
-      if ((tm[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(mat, ld3(P + 3 * a)));
-    __syncthreads();
   }
+  __syncthreads();
   if (bad) {
     if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
     return;

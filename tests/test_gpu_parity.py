@@ -176,6 +176,21 @@ def test_sub_apis_bit_exact(env):
     assert np.array_equal(c1, c2) and np.array_equal(a1, a2) and np.array_equal(s1, s2)
 
 
+def test_flatten_wide_library_and_near_ties_bit_exact(gpu_ctx):
+    """k_flatten_dep (candidate-dependent atom sets, filter sums, exact sums
+    for near ties) against the oracle's sequential flatten: a wide library
+    (0-12 rotors, 8-60 heavy atoms, rigid ligands included) and symmetric
+    ligands whose 180/120-degree partners tie up to rounding."""
+    smi = api.synthetic_smiles(1500, seed=4242, heavy=(8, 60), rot=(0, 12), grammar=1)
+    smi += ["c1ccc(cc1)-c1ccccc1", "CC(C)(C)c1ccc(cc1)C(F)(F)F", "c1ccc(cc1)Cc1ccccc1", "OC(=O)c1ccc(cc1)C(=O)O",
+            "c1cc(ccc1Cc1ccc(cc1)Cc1ccccc1)Cc1ccccc1", "FC(F)(F)CCC(F)(F)F", "C1CCC(CC1)CC1CCCCC1"]
+    raw = LigandBatch(api.prepare_smiles(smi, mode=1, nthreads=THREADS))
+    c1, a1, s1 = api.flatten(raw, 20, gpu_ctx)
+    c2, a2, s2 = Oracle("port").flatten(raw, 20, nthreads=THREADS)
+    assert np.array_equal(s1, s2)
+    assert np.array_equal(c1.view(np.uint64), c2.view(np.uint64)) and np.array_equal(a1, a2)
+
+
 def test_local_search_random_poses_bit_exact(env):
     ctx, pocket, host, b = env
     port = Oracle("port", trig=1)

@@ -36,3 +36,7 @@ for i in bad[:3]:
     t0, t1 = b.torsion_offset[i], b.torsion_offset[i + 1]
     print(i, "N", ligs[i].n_atoms, "m", ligs[i].n_torsions, "st", st[i], wst[i], "ang", np.round(ang[t0:t1], 4),
           np.round(wang[t0:t1], 4))
+    a0, a1 = b.atom_offset[i], b.atom_offset[i + 1]
+    d = np.abs(conf[a0:a1] - wconf[a0:a1])
+    print("   max |dconf|", d.max(), "rows", np.nonzero(d.max(1))[0][:10], "base==gpu", np.array_equal(conf[a0:a1], b.xyz[a0:a1]),
+          "base==oracle", np.array_equal(wconf[a0:a1], b.xyz[a0:a1]))
