@@ -608,6 +608,9 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         w = (1ull << kFC) - 1;
 #endif
         w |= 1ull << bo;
+#ifdef VS_FLAT_NO_EXACT  // timing experiments only: trust the filter blindly
+        w = 1ull << bo;
+#endif
         int best_off = bo;
         if (__popcll(w) > 1) {
           // exact sequential sums (transform.cpp:83-90) of the near-tied
