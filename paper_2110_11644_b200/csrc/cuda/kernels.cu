@@ -2,8 +2,10 @@
 //
 //   k_setup        per ligand: validation, heavy-atom list, right-set masks,
 //                  torsion dependency closures D_t (thread per ligand)
-//   k_flatten      flatten (search.cpp:27-69): CTA per ligand, one thread
-//                  per 10-degree candidate, sequential distance sums
+//   k_flatten_dep  flatten (search.cpp:27-69): CTA per ligand, 8 lanes per
+//                  10-degree candidate, candidate-dependent atoms only, exact
+//                  sequential sums for near ties (k_flatten: legacy layout,
+//                  used for ligands too large for its shared memory)
 //   k_search       initial_poses + local_search (search.cpp:84-193): one
 //                  warp per (ligand, restart), persistent, atomic work queue
 //   k_select       cluster_and_select + chem_score + argmax
