@@ -339,6 +339,21 @@ def test_large_flexible_ligands(env):
     assert np.array_equal(got.best_conformation, want["conformation"])
 
 
+def test_flatten_legacy_path_for_very_large_ligands(env):
+    """Ligands whose k_flatten_dep candidate buffer would exceed 200 KB of
+    shared memory (N > ~216 atoms) run the legacy one-thread-per-candidate
+    k_flatten; a batch mixing them with small ligands stays bit-exact."""
+    ctx, pocket, host, _ = env
+    big = "C1CCC(CC1)" * 13 + "C1CCCCC1"  # 14 cyclohexanes, 13 torsions, 226 atoms
+    smi = [big, "CCCCOc1ccccc1", big.replace("C1CCCCC1", "c1ccccc1")]
+    raw = LigandBatch(api.prepare_smiles(smi, mode=1, nthreads=THREADS))
+    assert raw.ligands[0].n_atoms > 216
+    c1, a1, s1 = api.flatten(raw, 20, ctx)
+    c2, a2, s2 = Oracle("port").flatten(raw, 20, nthreads=THREADS)
+    assert np.all(s1 == 0) and np.array_equal(s1, s2)
+    assert np.array_equal(c1.view(np.uint64), c2.view(np.uint64)) and np.array_equal(a1, a2)
+
+
 # ------------------------------------------------------------------ golden + tolerance
 def test_golden_config1_gpu(gpu_ctx):
     g = np.load(os.path.join(os.path.dirname(__file__), "golden", "config1.npz"))
