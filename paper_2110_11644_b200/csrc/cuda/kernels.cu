@@ -384,7 +384,8 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   uint32_t *tmr = tms + nmax;                                 // right-set mask of rank r
   int *tax = reinterpret_cast<int *>(tmr + nmax);             // torsion u's axis atoms, ea | eb << 16
   __shared__ int idx[VS_MAX_TORSIONS + 1];
-  __shared__ int changed, bad, sweeps_done, s_nd, s_nn;
+  __shared__ int changed, bad, sweeps_done, s_nd, s_nn, s_ver, s_skip;
+  __shared__ int stamp[VS_MAX_TORSIONS + 1];
   __shared__ uint32_t s_dt, s_du;
   __shared__ double s_ib;
   const double *base = b.xyz + 3 * (size_t)a0;
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
   if (tid < m) {
     idx[tid] = 0;
+    stamp[tid] = -1;
     const int bi = b.tors_bond[t0 + tid], b0 = b.bond_off[l];
     tax[tid] = b.bond_a[b0 + bi] | (b.bond_b[b0 + bi] << 16);
   }
@@ -401,6 +403,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   if (tid == 0) {
     bad = 0;
     sweeps_done = 0;
+    s_ver = 0;
   }
   __syncthreads();
   for (int sweep = 0; sweep < max_sweeps && m > 0; ++sweep) {
@@ -412,8 +415,15 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
     for (int i = tid; i < 3 * N; i += blockDim.x) P[i] = base[i];
     __syncthreads();
     for (int t = 0; t < m; ++t) {
-      // ---- A (warp 0): D_t, the common positions, the shared matrices
-      if (tid < 32) {
+      // ---- A (warp 0): D_t, the common positions, the shared matrices.
+      // If no lattice index changed since torsion t's last decision, its 36
+      // candidates are the same conformations as then, cyclically shifted so
+      // that the previous winner sits at offset 0: the first argmax is 0 and
+      // the evaluation is skipped (only the prefix advances).
+      if (tid < 32 && stamp[t] == s_ver) {
+        if (lane == 0) s_skip = 1;
+      } else if (tid < 32) {
+        if (lane == 0) s_skip = 0;
         uint32_t dt = 1u << t;
         for (int u = t + 1; u < m; ++u) {
           const int ax = tax[u];
@@ -486,6 +496,8 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
       }
       __syncthreads();
       if (bad) break;
+      const bool skipping = s_skip;
+      if (!skipping) {
       // ---- B: this lane's share of its candidate's D_t atoms through t..m-1
       const int nd = s_nd, nn = s_nn;
       const uint32_t dt = s_dt, du = s_du;
@@ -578,10 +590,13 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         if (g == 0) spread[o] = acc;
       }
-      __syncthreads();
+      }  // !skipping
+      __syncthreads();  // (skipping: every thread has read bad and s_skip)
       // ---- D (warp 0): certain winner, or the exact sums of the candidates
       // within rounding of it; then the prefix advance (search.cpp:52-60)
       if (tid < 32) {
+        int best_off = 0;
+        if (!skipping) {
         // first argmax (the reference's strict > from -inf; NaN never wins)
         const double v0 = spread[lane], v1 = lane + 32 < kFC ? spread[lane + 32] : ninf;
         double bv = v0 == v0 ? v0 : ninf;
@@ -613,7 +628,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
 #ifdef VS_FLAT_NO_EXACT  // timing experiments only: trust the filter blindly
         w = 1ull << bo;
 #endif
-        int best_off = bo;
+        best_off = bo;
         if (__popcll(w) > 1) {
           // exact sequential sums (transform.cpp:83-90) of the near-tied
           // candidates, first argmax among them
@@ -650,11 +665,16 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           }
           best_off = ev == ninf ? 0 : eo;
         }
+        }  // !skipping
         const int nidx = (idx[t] + best_off) % 36;
         __syncwarp();
-        if (lane == 0 && best_off != 0) {
-          idx[t] = nidx;
-          changed = 1;
+        if (lane == 0) {
+          if (best_off != 0) {
+            idx[t] = nidx;
+            changed = 1;
+            ++s_ver;
+          }
+          stamp[t] = s_ver;
         }
         const int ax = tax[t];
         double M[12], s, c;
