@@ -498,98 +498,98 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
       if (bad) break;
       const bool skipping = s_skip;
       if (!skipping) {
-      // ---- B: this lane's share of its candidate's D_t atoms through t..m-1
-      const int nd = s_nd, nn = s_nn;
-      const uint32_t dt = s_dt, du = s_du;
-      for (int r = g; r < nd; r += kFL) {
-        const int a = dl[r];
+        // ---- B: this lane's share of its candidate's D_t atoms through t..m-1
+        const int nd = s_nd, nn = s_nn;
+        const uint32_t dt = s_dt, du = s_du;
+        for (int r = g; r < nd; r += kFL) {
+          const int a = dl[r];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) Co[(3 * r + c) * kFC] = P[3 * a + c];
-      }
-      __syncwarp();
-      for (int u = t; u < m; ++u) {
-        if (!(((du | dt) >> u) & 1u)) continue;  // candidate-independent and moves no D_t atom
-        double M[12];
-        if ((dt >> u) & 1u) {
-          const int ax = tax[u], ea = ax & 0xffff, eb = ax >> 16;
-          d3 pa, pb;
-          if (u == t) {
-            pa = ld3(P + 3 * ea);
-            pb = ld3(P + 3 * eb);
-          } else {
-            const int sa = slot[ea], sb = slot[eb];
-            pa = sa >= 0 ? d3{Co[(3 * sa) * kFC], Co[(3 * sa + 1) * kFC], Co[(3 * sa + 2) * kFC]} : ld3(AX + 6 * u);
-            pb = sb >= 0 ? d3{Co[(3 * sb) * kFC], Co[(3 * sb + 1) * kFC], Co[(3 * sb + 2) * kFC]}
-                         : ld3(AX + 6 * u + 3);
-          }
-          double s, c;
-          lattice_sc(u == t ? (idx[t] + o) % 36 : idx[u], s, c);
-          if (!torsion_setup(pa, pb, s, c, M)) bad = 1;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 12; ++k) M[k] = Ms[12 * u + k];
+          for (int c = 0; c < 3; ++c) Co[(3 * r + c) * kFC] = P[3 * a + c];
         }
-        __syncwarp();  // endpoints read before anyone moves them
-        for (int r = g; r < nd; r += kFL)
-          if ((tmr[r] >> u) & 1u) {
-            double *x = Co + 3 * r * kFC;
-            const d3 y = torsion_apply(M, d3{x[0], x[kFC], x[2 * kFC]});
-            x[0] = y.x;
-            x[kFC] = y.y;
-            x[2 * kFC] = y.z;
-          }
         __syncwarp();
-      }
-      // ---- C: filter sum over the pairs that touch D_t, in two flattened
-      // walks strided by the 8 lanes of the candidate: (rank r, common k),
-      // then (rank r, rank s > r).
-      {
-        double acc = 0.0;
-        if (nn > 0) {
-          int r = g / nn, k = g - r * nn;
-          d3 xi{0.0, 0.0, 0.0};
-          if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
-          while (r < nd) {
-            const double *q = Qc + 4 * k;
-            acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[1], q[2]})));
-            k += kFL;
-            if (k >= nn) {
-              do {
-                k -= nn;
-                ++r;
-              } while (k >= nn);
-              if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+        for (int u = t; u < m; ++u) {
+          if (!(((du | dt) >> u) & 1u)) continue;  // candidate-independent and moves no D_t atom
+          double M[12];
+          if ((dt >> u) & 1u) {
+            const int ax = tax[u], ea = ax & 0xffff, eb = ax >> 16;
+            d3 pa, pb;
+            if (u == t) {
+              pa = ld3(P + 3 * ea);
+              pb = ld3(P + 3 * eb);
+            } else {
+              const int sa = slot[ea], sb = slot[eb];
+              pa = sa >= 0 ? d3{Co[(3 * sa) * kFC], Co[(3 * sa + 1) * kFC], Co[(3 * sa + 2) * kFC]} : ld3(AX + 6 * u);
+              pb = sb >= 0 ? d3{Co[(3 * sb) * kFC], Co[(3 * sb + 1) * kFC], Co[(3 * sb + 2) * kFC]}
+                           : ld3(AX + 6 * u + 3);
             }
+            double s, c;
+            lattice_sc(u == t ? (idx[t] + o) % 36 : idx[u], s, c);
+            if (!torsion_setup(pa, pb, s, c, M)) bad = 1;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) M[k] = Ms[12 * u + k];
           }
+          __syncwarp();  // endpoints read before anyone moves them
+          for (int r = g; r < nd; r += kFL)
+            if ((tmr[r] >> u) & 1u) {
+              double *x = Co + 3 * r * kFC;
+              const d3 y = torsion_apply(M, d3{x[0], x[kFC], x[2 * kFC]});
+              x[0] = y.x;
+              x[kFC] = y.y;
+              x[2 * kFC] = y.z;
+            }
+          __syncwarp();
         }
+        // ---- C: filter sum over the pairs that touch D_t, in two flattened
+        // walks strided by the 8 lanes of the candidate: (rank r, common k),
+        // then (rank r, rank s > r).
         {
-          int r = 0, k = g, len = nd - 1;
-          while (r < nd - 1 && k >= len) {
-            k -= len;
-            ++r;
-            len = nd - 1 - r;
-          }
-          d3 xi{0.0, 0.0, 0.0};
-          if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
-          while (r < nd - 1) {
-            const double *q = Co + 3 * (r + 1 + k) * kFC;
-            acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
-            k += kFL;
-            if (k >= len) {
-              do {
-                k -= len;
-                ++r;
-                len = nd - 1 - r;
-              } while (r < nd - 1 && k >= len);
-              if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+          double acc = 0.0;
+          if (nn > 0) {
+            int r = g / nn, k = g - r * nn;
+            d3 xi{0.0, 0.0, 0.0};
+            if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+            while (r < nd) {
+              const double *q = Qc + 4 * k;
+              acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[1], q[2]})));
+              k += kFL;
+              if (k >= nn) {
+                do {
+                  k -= nn;
+                  ++r;
+                } while (k >= nn);
+                if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+              }
             }
           }
+          {
+            int r = 0, k = g, len = nd - 1;
+            while (r < nd - 1 && k >= len) {
+              k -= len;
+              ++r;
+              len = nd - 1 - r;
+            }
+            d3 xi{0.0, 0.0, 0.0};
+            if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+            while (r < nd - 1) {
+              const double *q = Co + 3 * (r + 1 + k) * kFC;
+              acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
+              k += kFL;
+              if (k >= len) {
+                do {
+                  k -= len;
+                  ++r;
+                  len = nd - 1 - r;
+                } while (r < nd - 1 && k >= len);
+                if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+              }
+            }
+          }
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+          if (g == 0) spread[o] = acc;
         }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        if (g == 0) spread[o] = acc;
-      }
       }  // !skipping
       __syncthreads();  // (skipping: every thread has read bad and s_skip)
       // ---- D (warp 0): certain winner, or the exact sums of the candidates
@@ -597,74 +597,74 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
       if (tid < 32) {
         int best_off = 0;
         if (!skipping) {
-        // first argmax (the reference's strict > from -inf; NaN never wins)
-        const double v0 = spread[lane], v1 = lane + 32 < kFC ? spread[lane + 32] : ninf;
-        double bv = v0 == v0 ? v0 : ninf;
-        int bo = lane;
-        if (v1 > bv) {
-          bv = v1;
-          bo = lane + 32;
-        }
-#pragma unroll
-        for (int sh = 16; sh; sh >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, sh);
-          const int oo = __shfl_xor_sync(0xffffffffu, bo, sh);
-          if (ov > bv || (ov == bv && oo < bo)) {
-            bv = ov;
-            bo = oo;
-          }
-        }
-        if (bv == ninf) bo = 0;
-        const double ib2 = 2.0 * s_ib;
-        const bool n0 = lane != bo && !(bv - v0 > (ib2 + bv + v0) * npairs * 0x1p-49 + 0x1p-900);
-        const bool n1 = lane + 32 < kFC && lane + 32 != bo &&
-                        !(bv - v1 > (ib2 + bv + v1) * npairs * 0x1p-49 + 0x1p-900);
-        unsigned long long w = (unsigned long long)__ballot_sync(0xffffffffu, n0) |
-                               ((unsigned long long)__ballot_sync(0xffffffffu, n1) << 32);
-#ifdef VS_FLAT_FORCE_EXACT
-        w = (1ull << kFC) - 1;
-#endif
-        w |= 1ull << bo;
-#ifdef VS_FLAT_NO_EXACT  // timing experiments only: trust the filter blindly
-        w = 1ull << bo;
-#endif
-        best_off = bo;
-        if (__popcll(w) > 1) {
-          // exact sequential sums (transform.cpp:83-90) of the near-tied
-          // candidates, first argmax among them
-          double ev = ninf;
-          int eo = lane;
-          for (int q = lane; q < kFC; q += 32) {
-            if (!((w >> q) & 1ull)) continue;
-            const double *Ct = C + q;
-            double sum = 0.0;
-            for (int i = 0; i + 1 < N; ++i) {
-              const int si = slot[i];
-              const d3 xi = si >= 0 ? d3{Ct[(3 * si) * kFC], Ct[(3 * si + 1) * kFC], Ct[(3 * si + 2) * kFC]}
-                                    : ld3(Q + 3 * i);
-              for (int j = i + 1; j < N; ++j) {
-                const int sj = slot[j];
-                const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
-                                      : ld3(Q + 3 * j);
-                sum += dsqrt_dist2(sqn3(sub3(xi, xj)));
-              }
-            }
-            if (sum > ev) {
-              ev = sum;
-              eo = q;
-            }
+          // first argmax (the reference's strict > from -inf; NaN never wins)
+          const double v0 = spread[lane], v1 = lane + 32 < kFC ? spread[lane + 32] : ninf;
+          double bv = v0 == v0 ? v0 : ninf;
+          int bo = lane;
+          if (v1 > bv) {
+            bv = v1;
+            bo = lane + 32;
           }
 #pragma unroll
           for (int sh = 16; sh; sh >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, ev, sh);
-            const int oo = __shfl_xor_sync(0xffffffffu, eo, sh);
-            if (ov > ev || (ov == ev && oo < eo)) {
-              ev = ov;
-              eo = oo;
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, sh);
+            const int oo = __shfl_xor_sync(0xffffffffu, bo, sh);
+            if (ov > bv || (ov == bv && oo < bo)) {
+              bv = ov;
+              bo = oo;
             }
           }
-          best_off = ev == ninf ? 0 : eo;
-        }
+          if (bv == ninf) bo = 0;
+          const double ib2 = 2.0 * s_ib;
+          const bool n0 = lane != bo && !(bv - v0 > (ib2 + bv + v0) * npairs * 0x1p-49 + 0x1p-900);
+          const bool n1 = lane + 32 < kFC && lane + 32 != bo &&
+                          !(bv - v1 > (ib2 + bv + v1) * npairs * 0x1p-49 + 0x1p-900);
+          unsigned long long w = (unsigned long long)__ballot_sync(0xffffffffu, n0) |
+                                 ((unsigned long long)__ballot_sync(0xffffffffu, n1) << 32);
+#ifdef VS_FLAT_FORCE_EXACT
+          w = (1ull << kFC) - 1;
+#endif
+          w |= 1ull << bo;
+#ifdef VS_FLAT_NO_EXACT  // timing experiments only: trust the filter blindly
+          w = 1ull << bo;
+#endif
+          best_off = bo;
+          if (__popcll(w) > 1) {
+            // exact sequential sums (transform.cpp:83-90) of the near-tied
+            // candidates, first argmax among them
+            double ev = ninf;
+            int eo = lane;
+            for (int q = lane; q < kFC; q += 32) {
+              if (!((w >> q) & 1ull)) continue;
+              const double *Ct = C + q;
+              double sum = 0.0;
+              for (int i = 0; i + 1 < N; ++i) {
+                const int si = slot[i];
+                const d3 xi = si >= 0 ? d3{Ct[(3 * si) * kFC], Ct[(3 * si + 1) * kFC], Ct[(3 * si + 2) * kFC]}
+                                      : ld3(Q + 3 * i);
+                for (int j = i + 1; j < N; ++j) {
+                  const int sj = slot[j];
+                  const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
+                                        : ld3(Q + 3 * j);
+                  sum += dsqrt_dist2(sqn3(sub3(xi, xj)));
+                }
+              }
+              if (sum > ev) {
+                ev = sum;
+                eo = q;
+              }
+            }
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, ev, sh);
+              const int oo = __shfl_xor_sync(0xffffffffu, eo, sh);
+              if (ov > ev || (ov == ev && oo < eo)) {
+                ev = ov;
+                eo = oo;
+              }
+            }
+            best_off = ev == ninf ? 0 : eo;
+          }
         }  // !skipping
         const int nidx = (idx[t] + best_off) % 36;
         __syncwarp();
