@@ -332,9 +332,10 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
 //     candidate and are only bounded (I <= (n_I - 1) * sum |q - q_0|).
 //   * The reference's choice is the first argmax of R_o = fl_seq(I + T_o).
 //     With n pairs, |R_o - (I + T_o)| <= gamma_n (I + T_o) and our A_o carries
-//     at most the same plus the 2^-50 of the filter square root, so
-//     A_best - A_o > (2 I_bound + A_best + A_o) * n * 2^-49 proves
-//     R_best > R_o.  Candidates that fail the test (near ties: symmetric
+//     at most the same plus the 2^-50 of the filter square root (and 2^-500
+//     absolute per pair: near-coincident atoms sample 0), so
+//     A_best - A_o > ((2 I_bound + A_best + A_o) * 2^-48 + 2^-499) * n proves
+//     R_best > R_o (the 2^-48 = 32 u covers 2 gamma_n + 2^-49 from n = 1 on).  Candidates that fail the test (near ties: symmetric
 //     groups, ~2% of decisions) get the exact sequential sum of the legacy
 //     kernel, and the argmax is taken over those exact values.
 // The decision, and so every output, is bit-identical to the legacy kernel.
@@ -616,9 +617,9 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           }
           if (bv == ninf) bo = 0;
           const double ib2 = 2.0 * s_ib;
-          const bool n0 = lane != bo && !(bv - v0 > (ib2 + bv + v0) * npairs * 0x1p-49 + 0x1p-900);
+          const bool n0 = lane != bo && !(bv - v0 > ((ib2 + bv + v0) * 0x1p-48 + 0x1p-499) * npairs);
           const bool n1 = lane + 32 < kFC && lane + 32 != bo &&
-                          !(bv - v1 > (ib2 + bv + v1) * npairs * 0x1p-49 + 0x1p-900);
+                          !(bv - v1 > ((ib2 + bv + v1) * 0x1p-48 + 0x1p-499) * npairs);
           unsigned long long w = (unsigned long long)__ballot_sync(0xffffffffu, n0) |
                                  ((unsigned long long)__ballot_sync(0xffffffffu, n1) << 32);
 #ifdef VS_FLAT_FORCE_EXACT  // testing only: exact sums for every candidate
