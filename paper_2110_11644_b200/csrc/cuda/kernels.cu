@@ -359,6 +359,9 @@ size_t flatten_dep_smem(int nmax, int mmax) {
          (size_t)(5 * nmax + mmax) * sizeof(int);
 }
 
+#ifndef VS_FLAT_ROWS
+#define VS_FLAT_ROWS 1  // cross pairs: whole rows per lane (4 distances in flight) before the strided walk
+#endif
 #ifndef VS_FLAT_MINB
 #define VS_FLAT_MINB 3  // 3 CTAs (27 warps) per SM: 72 registers; without the cap 92 (2 CTAs) measured 35% slower
 #endif
@@ -546,8 +549,33 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         // then (rank r, rank s > r).
         {
           double acc = 0.0;
+#if VS_FLAT_ROWS
+          // full rows first: lane g takes ranks g, g + 8, ... of the first
+          // 8 * floor(nd / 8) and walks all nn common atoms, four at a time
+          const int nd8 = nd & ~(kFL - 1);
+          if (nn > 0)
+            for (int r = g; r < nd8; r += kFL) {
+              const d3 xi{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+              int k = 0;
+              for (; k + 4 <= nn; k += 4) {
+                double d[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const double *q = Qc + 4 * (k + e);
+                  d[e] = dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[1], q[2]})));
+                }
+                acc += (d[0] + d[1]) + (d[2] + d[3]);
+              }
+              for (; k < nn; ++k) {
+                const double *q = Qc + 4 * k;
+                acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[1], q[2]})));
+              }
+            }
+#else
+          const int nd8 = 0;
+#endif
           if (nn > 0) {
-            int r = g / nn, k = g - r * nn;
+            int r = nd8 + g / nn, k = g - (g / nn) * nn;
             d3 xi{0.0, 0.0, 0.0};
             if (r < nd) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
             while (r < nd) {
