@@ -671,7 +671,22 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
                 const int si = slot[i];
                 const d3 xi = si >= 0 ? d3{Ct[(3 * si) * kFC], Ct[(3 * si + 1) * kFC], Ct[(3 * si + 2) * kFC]}
                                       : ld3(Q + 3 * i);
-                for (int j = i + 1; j < N; ++j) {
+                int j = i + 1;
+                for (; j + 3 < N; j += 4) {  // four distances in flight, added in order
+                  double d[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int sj = slot[j + e];
+                    const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
+                                          : ld3(Q + 3 * (j + e));
+                    d[e] = dsqrt_dist2(sqn3(sub3(xi, xj)));
+                  }
+                  sum += d[0];
+                  sum += d[1];
+                  sum += d[2];
+                  sum += d[3];
+                }
+                for (; j < N; ++j) {
                   const int sj = slot[j];
                   const d3 xj = sj >= 0 ? d3{Ct[(3 * sj) * kFC], Ct[(3 * sj + 1) * kFC], Ct[(3 * sj + 2) * kFC]}
                                         : ld3(Q + 3 * j);
