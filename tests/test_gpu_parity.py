@@ -326,6 +326,27 @@ def test_edge_cases_statuses_and_mixed_batch(env):
     assert r1.results["status"][0] == 0 and r1.results["best_score"][0] == w1["results"]["best_score"][0]
 
 
+def test_flatten_degenerate_axis_in_each_phase(gpu_ctx):
+    """A degenerate torsion axis is reported whichever k_flatten_dep phase
+    meets it first: the candidates' own torsion (per-candidate build), a
+    later torsion whose axis moves with the candidate, or a later
+    candidate-independent torsion (warp 0's common pass); same status as
+    the oracle."""
+    # torsion 0 on bond (1,2), right {2,3}; torsion 1 on bond (0,4), whose
+    # endpoints coincide and do not move with torsion 0 (independent)
+    indep = _lig("indep", [[0, 0, 0], [1, 0, 0], [2, 0, 0], [2, 1, 0], [0, 0, 0], [-1, 1, 0]], [0] * 6, [1] * 6,
+                 bonds=[(0, 1), (1, 2), (2, 3), (0, 4), (4, 5)], tors=[1, 3], rights=[[2, 3], [4, 5]])
+    # torsion 1 on bond (2,3) inside right(0): its axis moves with torsion 0
+    dep = _lig("dep", [[0, 0, 0], [1, 0, 0], [2, 0, 0], [2, 0, 0], [3, 1, 0]], [0] * 5, [1] * 5,
+               bonds=[(0, 1), (1, 2), (2, 3), (3, 4)], tors=[1, 2], rights=[[2, 3, 4], [3, 4]])
+    fine = api.prepare_smiles(["CCCCOc1ccccc1"], mode=1)[0]
+    raw = LigandBatch([indep, fine, dep])
+    _, _, s1 = api.flatten(raw, 20, gpu_ctx)
+    _, _, s2 = Oracle("port").flatten(raw, 20)
+    assert s1[0] == abi.VS_LIG_DEGENERATE_AXIS and s1[2] == abi.VS_LIG_DEGENERATE_AXIS and s1[1] == 0
+    assert np.array_equal(s1, s2)
+
+
 def test_large_flexible_ligands(env):
     ctx, pocket, host, _ = env
     smi = api.synthetic_smiles(12, seed=123, heavy=(55, 80), rot=(10, 15))
