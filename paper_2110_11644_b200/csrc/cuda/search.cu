@@ -55,6 +55,9 @@ constexpr int kWarps = VS_SEARCH_WARPS;
   do {              \
   } while (0)
 #endif
+#ifndef VS_ROW_SELECT
+#define VS_ROW_SELECT 1  // torsion rows read non-D_t atoms from vcur instead of completing the rows
+#endif
 #ifndef VS_TORSH_SMEM
 #define VS_TORSH_SMEM 1  // heavy atoms' torsioned frame also in shared memory (0: read it from the
                          // global frame -- measured 2% slower; frees 3n doubles per warp)
@@ -777,6 +780,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
             vb[row * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, col), out);
           }
         }
+#if !VS_ROW_SELECT
         if (grp != 0) {
           // heavy atoms outside D_t sample exactly as in the current pose:
           // complete the torsion rows with the current values
@@ -788,6 +792,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
               if (!((s_dm[h] >> t) & 1u)) vb[rr * nmax + h] = vcur[h];
           }
         }
+#endif
         __syncwarp();
         PH(grp == 0 ? 2 : 3)
         // geo_score of each neighbour in the group (grid.cpp:97-101)
@@ -795,8 +800,19 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         if (lane < jn) {
           const double *row = vb + lane * nmax;
           double acc = 0.0;
-          #pragma unroll 4
-          for (int h = 0; h < n; ++h) acc += row[h];
+#if VS_ROW_SELECT
+          if (grp != 0) {
+            // heavy atoms outside D_t sample exactly as in the current pose:
+            // their values come from vcur (the row holds only D_t's samples)
+            const uint32_t tb = 1u << (tlo + (lane >> 1));
+            #pragma unroll 4
+            for (int h = 0; h < n; ++h) acc += (s_dm[h] & tb) ? row[h] : vcur[h];
+          } else
+#endif
+          {
+            #pragma unroll 4
+            for (int h = 0; h < n; ++h) acc += row[h];
+          }
           gacc = acc;
         }
         // first strict maximum of the group, then against the running best
@@ -814,8 +830,14 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
           bv = gv;
           bj = j0 + gj;
           const double *row = vb + gj * nmax;
+#if VS_ROW_SELECT
+          const uint32_t tb = grp != 0 ? 1u << (tlo + (gj >> 1)) : 0xffffffffu;
+          #pragma unroll 1
+          for (int h = lane; h < n; h += 32) vbest[h] = (grp == 0 || (s_dm[h] & tb)) ? row[h] : vcur[h];
+#else
           #pragma unroll 1
           for (int h = lane; h < n; h += 32) vbest[h] = row[h];
+#endif
         }
         __syncwarp();
         PH(4)
