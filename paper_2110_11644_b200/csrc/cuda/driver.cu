@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -160,11 +161,18 @@ void ensure_lattice(int device) {
 
 int chem_class(uint8_t e) { return e == VS_ELEM_C ? 0 : ((e == VS_ELEM_N || e == VS_ELEM_O) ? 1 : 2); }
 
+// 1 A cells: 64% of the listed atoms lie within 4.5 A of a point of the cell
+// (2 A: 43%); k_select -12% against 2 A cells (measured), lists stay L2-sized
+constexpr double kChemCell = 1.0;
+
 // Culling cells for chem_score: every protein atom whose distance to the
 // cell's box is below 4.5 A (+1e-6 margin), listed in protein order.
 vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
   const double cutoff = 4.5 + 1e-6;
-  const double cs = 2.0;
+  // cell edge: smaller cells list fewer atoms beyond 4.5 A per cell (A/B
+  // override VSDOCK_CHEM_CELL, development only)
+  double cs = kChemCell;
+  if (const char *e = std::getenv("VSDOCK_CHEM_CELL")) cs = std::atof(e) > 0.25 ? std::atof(e) : cs;
   double lo[3], hi[3];
   for (int a = 0; a < 3; ++a) {
     lo[a] = p->origin[a] - 5.0;

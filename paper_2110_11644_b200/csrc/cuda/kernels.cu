@@ -816,6 +816,8 @@ __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, dou
   for (int q = lo; q < hi; ++q) {
     const int j = list ? __ldg(list + q) : q;
     const d3 pp{__ldg(p.pxyz + 3 * j), __ldg(p.pxyz + 3 * j + 1), __ldg(p.pxyz + 3 * j + 2)};
+    // (an exact d2 >= 20.25 early-out before the sqrt measured 6% slower:
+    // the lanes are different poses, so the branch only adds divergence)
     const double d = dsqrt(sqn3(sub3(x, pp)));
     if (d >= 4.5) continue;
     ++pairs;
