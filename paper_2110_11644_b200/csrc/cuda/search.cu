@@ -326,12 +326,18 @@ __device__ __noinline__ void full_conformation(double *out, const double *S, int
 
 // Pivot = centroid of apply_rigid(tors, T) (search.cpp:124): the warp writes
 // the transformed conformation to `scratch`, then three lanes run the
-// Eigen-order row sums (dmath.cuh centroid_row).
+// Eigen-order row sums (dmath.cuh centroid_row).  `rows`: the coordinates
+// that can have changed since the last pivot (a translation along one axis
+// leaves the other coordinates of every atom, hence their rows, bit-identical;
+// row 2 is the long sequential sum, so x/y moves skip it).
+#ifndef VS_PIVOT_ROWS
+#define VS_PIVOT_ROWS 1
+#endif
 __device__ __forceinline__ void compute_pivot(double *scratch, double *S, int N, const double *hx, bool rigid,
-                                              int lane) {
+                                              int lane, unsigned rows = 7u) {
   full_conformation(scratch, S, N, hx, rigid, lane);
   __syncwarp();
-  if (lane < 3) S[S_PIV + lane] = centroid_row(scratch, N, lane);
+  if (lane < 3 && ((rows >> lane) & 1u)) S[S_PIV + lane] = centroid_row(scratch, N, lane);
   __syncwarp();
 }
 
@@ -899,7 +905,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args
         if (lane == 0) S[S_GEO] = bv;
         __syncwarp();
         // new pivot = centroid of the adopted conformation (vb is free here)
-        compute_pivot(vb, S, N, hx, true, lane);
+        compute_pivot(vb, S, N, hx, true, lane, VS_PIVOT_ROWS && bj < 6 ? 1u << (bj >> 1) : 7u);
         PH(bj < 12 ? 5 : 6)
       } else {
         if (lane == 0) {
