@@ -342,7 +342,10 @@ __device__ __forceinline__ void compute_pivot(double *scratch, double *S, int N,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) k_search(search_args A) {
+#ifndef VS_SEARCH_MINB
+#define VS_SEARCH_MINB (16 / kWarps)  // A/B only: a higher count caps the registers (96 at 10: +9% search time)
+#endif
+__global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_args A) {
   extern __shared__ __align__(16) double sm[];
   // palette (CTA-wide): MODE 2 reads the 16 values; MODE 1 a table of code
   // pairs, entry i = (palette[i & 3], palette[i >> 2]), so two corners of a
