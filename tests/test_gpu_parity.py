@@ -212,6 +212,51 @@ def test_local_search_random_poses_bit_exact(env):
     assert np.array_equal(g[1], o[1]) and np.array_equal(g[2], o[2]) and np.array_equal(g[3], o[3])
 
 
+def test_local_search_node_box_faces_bit_exact(gpu_ctx):
+    """k_search's sampler decides "outside the node box" (grid.cpp:63-66) from
+    integer floor/ceil conversions (dmath.cuh field_value_fast): translation
+    neighbours landing exactly on each face of the box and 2^-40 beyond it,
+    starts on the faces, on an f64-grid pocket and on a 3-value (packed 2-bit)
+    one, against the oracle's double comparisons; a NaN pose stays NaN."""
+    n = 9
+    three = np.zeros(n ** 3)
+    idx = np.arange(n ** 3)
+    three[(idx % n + (idx // n) % n + idx // (n * n)) % 2 == 0] = 1.0
+    three[0] = -10.0
+    port = Oracle("port", trig=1)
+    lig = api.parse_smiles("C")
+    assert lig.n_atoms == 1 and np.all(lig.xyz == 0.0)
+    eps = 2.0 ** -40
+    starts = []
+    for axis in range(3):
+        for v in (7.0, 7.0 + eps, 1.0, 1.0 - eps, 8.0, 0.0):
+            p = np.array([4.0, 4.0, 4.0])
+            p[axis] = v
+            starts.append(p)
+    cfg = abi.ScoringConfig()
+    for pk in (pyramid_pocket(n, 1.0), explicit_pocket((n, n, n), 1.0, three)):
+        b = LigandBatch([lig] * len(starts))
+        poses = np.zeros(len(starts), dtype=abi.POSE_DTYPE)
+        poses["rotation"] = [0.0, 0.0, 0.0, 1.0]
+        poses["translation"] = starts
+        conf = np.array(starts)
+        ang = np.zeros(0)
+        poses["geo_score"] = port.geo_score(pk, b, conf)[0]
+        g = api.local_search(pk, b, poses, ang, conf, cfg, gpu_ctx)
+        o = port.local_search(pk, b, cfg, poses, ang, conf)
+        assert np.array_equal(g[4], o[4]) and np.array_equal(g[3], o[3])
+        assert np.array_equal(g[0].view(np.uint8), o[0].view(np.uint8))
+        assert np.array_equal(g[2].view(np.uint64), o[2].view(np.uint64))
+        nanpose = poses[:1].copy()
+        nanpose["translation"] = [[np.nan, 4.0, 4.0]]
+        nconf = np.array([[np.nan, 4.0, 4.0]])
+        nanpose["geo_score"] = np.nan
+        gn = api.local_search(pk, LigandBatch([lig]), nanpose, ang, nconf, cfg, gpu_ctx)
+        on = port.local_search(pk, LigandBatch([lig]), cfg, nanpose, ang, nconf)
+        assert np.isnan(gn[0]["geo_score"][0]) and np.isnan(on[0]["geo_score"][0])
+        assert np.array_equal(gn[3], on[3]) and np.array_equal(gn[4], on[4])
+
+
 @pytest.mark.parametrize("k,rescored", [(8, 30), (1, 1), (5, 2), (30, 30)])
 def test_dock_bit_exact_vs_oracle(env, k, rescored):
     ctx, pocket, host, b = env
