@@ -363,7 +363,8 @@ size_t flatten_dep_smem(int nmax, int mmax) {
 #define VS_FLAT_ROWS 1  // cross pairs: whole rows per lane (4 distances in flight) before the strided walk
 #endif
 #ifndef VS_FLAT_MINB
-#define VS_FLAT_MINB 3  // 3 CTAs (27 warps) per SM: 72 registers; without the cap 92 (2 CTAs) measured 35% slower
+#define VS_FLAT_MINB 3  // 3 CTAs (27 warps) per SM: 72 registers; without the cap 92 (2 CTAs) measured 35% slower,
+                        // 4 (56 registers, 412 B spills) 3.5% slower
 #endif
 __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, int max_sweeps, flat_out f, int nmax,
                                                                    int mmax, const int *lig_index) {
