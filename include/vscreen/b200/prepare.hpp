@@ -18,4 +18,10 @@ Ligand prepare_smiles(const std::string &smiles, int mode = 1);
 // prepare_ligand: mode 1 + GPU flatten (+ quantise_to_wire when quantize).
 std::vector<Ligand> prepare_ligands(const std::vector<std::string> &smiles, bool quantize = true);
 
+// Device selection for the reference-API calls made by THIS thread (the
+// reference's W docker threads can each pin one GPU, pipeline.cpp:343-363).
+// Default: $VS_DEVICE, else 0.  One vs_context (stream) per device.
+void use_device(int device);
+int device_count();
+
 }  // namespace vscreen::b200

@@ -1,4 +1,5 @@
-// Drop-in for search.hpp:17-79, plus the batch entry point this build adds.
+// Drop-in for search.hpp:17-79 (every declaration, exhaustive_dock included),
+// plus the batch entry point this build adds.
 // dock_and_score / dock_and_score_batch / flatten / local_search run on the
 // B200 through libvsdock.so; results match the reference's (bit-exact up to
 // the correctly rounded torsion sin/cos).
@@ -29,6 +30,11 @@ Pose local_search(const Pocket &pocket, const Ligand &ligand, Pose pose, const S
 std::vector<Pose> cluster_and_select(const std::vector<Pose> &poses, const Ligand &ligand, double threshold,
                                      std::size_t top);
 DockResult dock_and_score(const Pocket &pocket, const Ligand &ligand, const ScoringConfig &config = {});
+// search.hpp:74-79: brute-force test oracle (0.25 A lattice x 512 Fibonacci
+// orientations, ties keep the earliest point then orientation); rigid
+// ligands of <= 5 atoms, pockets <= 16 A per side, else InvalidArgument.
+// Field values come from the B200 sampler; the scan order is the reference's.
+Pose exhaustive_dock(const Pocket &pocket, const Ligand &ligand);
 
 // B200 batch entry point (no reference counterpart; the reference docks one
 // ligand per call from W threads, pipeline.cpp:206-244).  Ligands that the

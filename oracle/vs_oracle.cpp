@@ -29,6 +29,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -238,7 +239,7 @@ Conf apply_rigid(const Conf &c, const RT &T) {
 V3 centroid(const Conf &c) {
   if (c.empty()) throw LigandError(VS_LIG_EMPTY, "empty conformation");
   const std::ptrdiff_t n = static_cast<std::ptrdiff_t>(c.size());
-  V3 s;
+  V3 s{};
   for (int r = 0; r < 2; ++r) {
     double p = c[0][r];
     const std::ptrdiff_t size4 = (n - 1) & ~std::ptrdiff_t(3);
@@ -473,6 +474,46 @@ RT compose(const RT &b, const RT &a) {
   return o;
 }
 
+#ifdef VSO_TRACE
+// Development analysis only: per neighbour the score, the current score and,
+// over its moved heavy-atom samples, the sum of the cells' L1 gradient bounds
+// (local units), their count and the smallest distance to a node-box face.
+FILE *g_trace = nullptr;
+void trace_neighbour(const Pocket &p, const Ligand &lig, const Conf &c, const Conf &cur, double score, double cs) {
+  if (!g_trace) return;
+  double gsum = 0.0, gmax = 0.0, minface = 1e9;
+  int nm = 0;
+  for (std::size_t i = 0; i < lig.n_atoms(); ++i) {
+    if (!lig.heavy[i]) continue;
+    if (std::memcmp(&c[i], &cur[i], sizeof(V3)) == 0) continue;
+    ++nm;
+    double l[3];
+    int ix[3];
+    for (int a = 0; a < 3; ++a) {
+      l[a] = (c[i][a] - p.origin[a]) / p.spacing;
+      minface = std::min(minface, std::min(std::fabs(l[a]), std::fabs(l[a] - (p.dims[a] - 1))));
+      ix[a] = std::max(0, std::min((int)std::floor(l[a]), p.dims[a] - 2));
+    }
+    bool out = false;
+    for (int a = 0; a < 3; ++a) out |= l[a] < 0 || l[a] > p.dims[a] - 1;
+    if (out) continue;
+    double v[8];
+    for (int q = 0; q < 8; ++q) v[q] = p.at(ix[0] + (q & 1), ix[1] + ((q >> 1) & 1), ix[2] + (q >> 2));
+    double g = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      double mx = 0.0;
+      for (int q = 0; q < 8; ++q)
+        if (!((q >> a) & 1)) mx = std::max(mx, std::fabs(v[q | (1 << a)] - v[q]));
+      g += mx;
+    }
+    gsum += g;
+    gmax += g > 0 ? 1.0 : 0.0;  // non-uniform moved samples
+  }
+  const double rec[6] = {score, cs, gsum, (double)nm, minface, gmax};
+  std::fwrite(rec, sizeof rec, 1, g_trace);
+}
+#endif
+
 // search.cpp:109-193.
 Pose local_search(const Pocket &p, const Ligand &lig, Pose pose, const vs_scoring_config &cfg,
                   Counters *cn) {
@@ -482,6 +523,12 @@ Pose local_search(const Pocket &p, const Ligand &lig, Pose pose, const vs_scorin
   Conf torsioned = apply_torsions(base, lig, pose.ang, cn);
   double step_t = cfg.step_translation, step_r = cfg.step_rotation, step_q = cfg.step_torsion;
   for (int iter = 0; iter < cfg.max_iterations && step_t >= cfg.min_translation; ++iter) {
+#ifdef VSO_TRACE
+    if (g_trace) {
+      const double rec[6] = {-1e300, (double)(12 + 2 * m), step_t, 0, 0, 0};
+      std::fwrite(rec, sizeof rec, 1, g_trace);
+    }
+#endif
     const V3 pivot = centroid(pose.conf);
     double best_score = pose.geo;
     bool improved = false;
@@ -491,6 +538,9 @@ Pose local_search(const Pocket &p, const Ligand &lig, Pose pose, const vs_scorin
     auto consider = [&](const RT &T, const std::vector<double> *ang, const Conf &frame) {
       const Conf conf = apply_rigid(frame, T);
       const double score = geo_score(p, lig, conf, cn);
+#ifdef VSO_TRACE
+      trace_neighbour(p, lig, conf, pose.conf, score, pose.geo);
+#endif
       if (score > best_score) {
         best_score = score;
         improved = true;
@@ -840,6 +890,13 @@ void vso_config_default(vs_scoring_config *c) {
 // docker workers, pipeline.cpp:346-363).  counters (may be NULL): 9 per
 // ligand in Appendix B order S, A_rigid, A_tors, R_build, P_flat, P_chem,
 // P_rmsd, clash_pairs, oob_samples.
+#ifdef VSO_TRACE
+void vso_trace_open(const char *path) { vso::g_trace = std::fopen(path, "wb"); }
+void vso_trace_close() {
+  if (vso::g_trace) std::fclose(vso::g_trace);
+  vso::g_trace = nullptr;
+}
+#endif
 int vso_dock_batch(const vs_pocket_desc *pd, const vs_ligand_batch *b, const vs_scoring_config *cfg,
                    int nthreads, vs_dock_result *res, double *best_angles, double *best_conf,
                    uint64_t *counters) {

@@ -43,16 +43,26 @@ void check(vs_status s, const char *what) {
   throw DeviceError(std::string(what) + ": " + last_error());
 }
 
+// One vs_context per device, created on first use.  The calling thread's
+// device is vscreen::b200::use_device() (thread-local), else $VS_DEVICE, else 0,
+// so W reference-style docker threads can spread over the GPUs of a box.
+constexpr int kMaxDevices = 64;
+thread_local int tl_device = -1;
+
+int current_device() {
+  if (tl_device >= 0) return tl_device;
+  const char *env = std::getenv("VS_DEVICE");
+  return env ? std::atoi(env) : 0;
+}
+
 vs_context *context() {
-  static std::once_flag once;
-  static vs_context *ctx = nullptr;
-  static vs_status st = VS_OK;
-  std::call_once(once, [] {
-    const char *env = std::getenv("VS_DEVICE");
-    st = vs_context_create(env ? std::atoi(env) : 0, &ctx);
-  });
-  check(st, "vs_context_create");
-  return ctx;
+  static std::mutex mu;
+  static vs_context *ctx[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) throw DeviceError("vscreen::b200: device index out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ctx[dev]) check(vs_context_create(dev, &ctx[dev]), "vs_context_create");
+  return ctx[dev];
 }
 
 // SoA packing of ligands (vs_ligand_batch) with optional coordinate override.
@@ -108,22 +118,55 @@ vs_scoring_config to_c(const ScoringConfig &c) {
           c.min_translation, c.max_iterations, c.flatten_max_sweeps};
 }
 
-// Device pockets, cached by object identity + shape fingerprint.
+// Device pockets, cached by CONTENT: the key is a 64-bit FNV-1a hash of the
+// grid values, origin, spacing, dims and protein atoms, and a hit is
+// confirmed against a stored copy of all of them, so a Pocket mutated in
+// place or a new Pocket at a recycled address is never served the old device
+// grid (the reference's own tests rebuild pockets per SUBCASE,
+// test_dockengine.cpp:215-240).  One entry set per device.
+struct PocketKey {
+  int device = 0;
+  std::vector<double> meta;  // origin (3), spacing, dims (3)
+  std::vector<double> values;
+  std::vector<uint8_t> el;
+  std::vector<double> xyz;
+  bool operator==(const PocketKey &o) const {
+    return device == o.device && meta == o.meta && el == o.el && values.size() == o.values.size() &&
+           xyz.size() == o.xyz.size() &&
+           std::memcmp(values.data(), o.values.data(), values.size() * sizeof(double)) == 0 &&
+           std::memcmp(xyz.data(), o.xyz.data(), xyz.size() * sizeof(double)) == 0;
+  }
+};
+
+uint64_t fnv1a(uint64_t h, const void *p, std::size_t n) {
+  const auto *b = static_cast<const unsigned char *>(p);
+  for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
 struct PocketCache {
   std::mutex mu;
-  std::map<std::tuple<const void *, const void *, std::size_t, std::size_t>, vs_pocket *> map;
+  std::multimap<uint64_t, std::pair<PocketKey, vs_pocket *>> map;
   vs_pocket *get(const Pocket &p) {
-    std::lock_guard<std::mutex> lock(mu);
-    const auto key = std::make_tuple(static_cast<const void *>(&p), static_cast<const void *>(p.values.data()),
-                                     p.values.size(), p.protein_atoms.size());
-    auto it = map.find(key);
-    if (it != map.end()) return it->second;
-    std::vector<uint8_t> el;
-    std::vector<double> xyz;
+    PocketKey k;
+    k.device = current_device();
+    k.meta = {p.origin[0], p.origin[1], p.origin[2], p.spacing, double(p.dims[0]), double(p.dims[1]),
+              double(p.dims[2])};
+    k.values = p.values;
     for (const ProteinAtom &a : p.protein_atoms) {
-      el.push_back(static_cast<uint8_t>(a.element));
-      xyz.insert(xyz.end(), {a.position.x(), a.position.y(), a.position.z()});
+      k.el.push_back(static_cast<uint8_t>(a.element));
+      k.xyz.insert(k.xyz.end(), {a.position.x(), a.position.y(), a.position.z()});
     }
+    uint64_t h = 1469598103934665603ull;
+    h = fnv1a(h, &k.device, sizeof k.device);
+    h = fnv1a(h, k.meta.data(), k.meta.size() * sizeof(double));
+    h = fnv1a(h, k.values.data(), k.values.size() * sizeof(double));
+    h = fnv1a(h, k.el.data(), k.el.size());
+    h = fnv1a(h, k.xyz.data(), k.xyz.size() * sizeof(double));
+    vs_context *ctx = context();
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto [it, end] = map.equal_range(h); it != end; ++it)
+      if (it->second.first == k) return it->second.second;
     vs_pocket_desc d{};
     for (int a = 0; a < 3; ++a) {
       d.origin[a] = p.origin[a];
@@ -131,17 +174,17 @@ struct PocketCache {
     }
     d.spacing = p.spacing;
     d.values = p.values.data();
-    d.n_protein = static_cast<int32_t>(el.size());
-    d.protein_element = el.empty() ? nullptr : el.data();
-    d.protein_xyz = xyz.empty() ? nullptr : xyz.data();
-    vs_pocket *h = nullptr;
-    check(vs_pocket_create(context(), &d, &h), "vs_pocket_create");
-    if (map.size() > 64) {  // bounded: drop everything (pockets are cheap to re-upload)
-      for (auto &kv : map) vs_pocket_destroy(kv.second);
+    d.n_protein = static_cast<int32_t>(k.el.size());
+    d.protein_element = k.el.empty() ? nullptr : k.el.data();
+    d.protein_xyz = k.xyz.empty() ? nullptr : k.xyz.data();
+    vs_pocket *hd = nullptr;
+    check(vs_pocket_create(ctx, &d, &hd), "vs_pocket_create");
+    if (map.size() >= 64) {  // bounded: drop everything (pockets are cheap to re-upload)
+      for (auto &kv : map) vs_pocket_destroy(kv.second.second);
       map.clear();
     }
-    map[key] = h;
-    return h;
+    map.emplace(h, std::make_pair(std::move(k), hd));
+    return hd;
   }
 };
 PocketCache &pockets() {
@@ -666,6 +709,13 @@ static std::vector<Ligand> prep_many(const std::vector<std::string> &smiles, int
 }
 
 Ligand prepare_smiles(const std::string &smiles, int mode) { return prep_many({smiles}, mode)[0]; }
+
+void use_device(int device) {
+  if (device < 0 || device >= kMaxDevices) throw InvalidArgument("use_device: device index out of range");
+  tl_device = device;
+}
+
+int device_count() { return vs_device_count(); }
 
 std::vector<Ligand> prepare_ligands(const std::vector<std::string> &smiles, bool quantize) {
   std::vector<Ligand> ligs = prep_many(smiles, 1);

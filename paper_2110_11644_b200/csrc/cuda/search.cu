@@ -628,7 +628,8 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
           X[axis] = S[S_T + axis] + sign * step_t;
         } else {  // rotations about the pivot (search.cpp:159-167)
           double *X = Rj + kRow * (lane - 6);
-          const double *sq = A.c.spin + 4 * (6 * level + (lane - 6));
+          // tables end at n_levels (<= 4096): deeper levels have step 0, equal to the last entry
+          const double *sq = A.c.spin + 4 * (6 * min(level, A.c.n_levels - 1) + (lane - 6));
           const quat spin{sq[0], sq[1], sq[2], sq[3]};
           const d3 piv = ld3(S + S_PIV);
           const d3 spin_t = sub3(piv, quat_rotate(spin, piv));
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
             // sin/cos of ang[t] +- step_q from the current double-double
             // values and the level's step table (vs_crtrig.h sincos_shift)
             const int t = v >> 1;
-            const double *st = A.c.stepsc + 4 * level;
+            const double *st = A.c.stepsc + 4 * min(level, A.c.n_levels - 1);
             const bool neg = v & 1;
             const vs_crtrig::dd sd{neg ? -st[0] : st[0], neg ? -st[1] : st[1]}, cd{st[2], st[3]};
             double an;
@@ -825,7 +826,9 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
           gacc = acc;
         }
         // first strict maximum of the group, then against the running best
-        double gv = lane < jn ? gacc : -__longlong_as_double(0x7ff0000000000000LL);
+        // a NaN score is never adopted (score > best is false, search.cpp:138):
+        // map it to -inf so every lane's reduction agrees
+        double gv = (lane < jn && !isnan(gacc)) ? gacc : -__longlong_as_double(0x7ff0000000000000LL);
         int gj = lane < jn ? lane : 0x7fffffff;
         for (int off = 16; off > 0; off >>= 1) {
           const double ov = __shfl_xor_sync(0xffffffffu, gv, off);

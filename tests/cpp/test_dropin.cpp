@@ -96,6 +96,59 @@ int main() {
   CHECK(best == batch[0].best_score);
   CHECK(counter.scoring_evals == batch[0].scoring_evals);
 
+  // exhaustive_dock KATs (test_dockengine.cpp:665-693)
+  auto flat_pocket = [](int nodes, double spacing) {
+    Pocket p;
+    p.id = "test";
+    p.spacing = spacing;
+    p.dims = {nodes, nodes, nodes};
+    p.values.assign(static_cast<std::size_t>(nodes) * nodes * nodes, 0.0);
+    return p;
+  };
+  const Ligand carbon = b200::prepare_smiles("C", 2);
+  {
+    Pocket p3 = flat_pocket(3, 0.5);
+    p3.values[p3.value_index(2, 1, 0)] = 7.0;
+    const Pose pose = exhaustive_dock(p3, carbon);
+    CHECK((pose.conformation.col(0) - Eigen::Vector3d(1.0, 0.5, 0.0)).norm() < 1e-12);
+    CHECK(std::fabs(pose.geo_score - 7.0) <= 7e-12);
+    Pocket p2 = flat_pocket(2, 0.5);
+    p2.values[p2.value_index(0, 0, 0)] = 3.0;
+    p2.values[p2.value_index(1, 1, 1)] = 3.0;
+    CHECK((exhaustive_dock(p2, carbon).conformation.col(0) - Eigen::Vector3d(0, 0, 0)).norm() < 1e-12);
+    int limits = 0;
+    try { exhaustive_dock(p3, b200::prepare_smiles("CCO", 1)); } catch (const InvalidArgument &) { ++limits; }
+    try { exhaustive_dock(p3, b200::prepare_smiles("CCCC", 2)); } catch (const InvalidArgument &) { ++limits; }
+    try { exhaustive_dock(flat_pocket(35, 0.5), carbon); } catch (const InvalidArgument &) { ++limits; }
+    CHECK(limits == 3);
+  }
+
+  // device pockets are cached by content: a Pocket rebuilt at the same
+  // address with the same sizes, or mutated in place, is re-uploaded
+  // (test_dockengine.cpp:215-240 rebuilds `pocket` per SUBCASE)
+  {
+    Conformation origin(3, 1);
+    origin.col(0) = Eigen::Vector3d(0, 0, 0);
+    const double want[3] = {0.4, 0.0, 0.4 * 0.5};
+    const double zs[3] = {3.0, 4.5, 4.0};
+    for (int sc = 0; sc < 3; ++sc) {
+      Pocket pk = flat_pocket(2, 1.0);
+      pk.protein_atoms = {{Element::C, Eigen::Vector3d(0.0, 0.0, zs[sc])}};
+      CHECK(std::fabs(chem_score(pk, carbon, origin) - want[sc]) <= 1e-12);
+    }
+    Pocket pm = flat_pocket(3, 0.5);
+    const Conformation mid = [] { Conformation c(3, 1); c.col(0) = Eigen::Vector3d(0.5, 0.5, 0.5); return c; }();
+    CHECK(pocket_field_value(pm, mid.col(0)) == 0.0);
+    pm.values[pm.value_index(1, 1, 1)] = 5.0;  // mutated in place: same buffer, same sizes
+    CHECK(pocket_field_value(pm, mid.col(0)) == 5.0);
+  }
+
+  // per-thread device selection
+  CHECK(b200::device_count() >= 1);
+  b200::use_device(b200::device_count() - 1);
+  CHECK(dock_and_score(twin, co, cfg).best_score == a.best_score);
+  b200::use_device(0);
+
   std::printf(failures == 0 ? "ALL OK\n" : "%d FAILURES\n", failures);
   return failures == 0 ? 0 : 1;
 }

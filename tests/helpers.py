@@ -79,3 +79,72 @@ def rel_err(a, b) -> np.ndarray:
 
 
 PI = math.pi
+
+
+# ------------------------------------------------------------------ golden parity
+def load_golden(name: str):
+    """A fixture written by tests/golden/make_golden.py from oracle/_ref."""
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name))
+
+
+def golden_pocket(g) -> Pocket:
+    return Pocket(g["pocket_origin"], float(g["pocket_spacing"]), tuple(g["pocket_dims"]),
+                  g["pocket_values_code"].astype(np.float64), g["protein_element"], g["protein_xyz"], id="golden")
+
+
+def heavy_rmsd_per_ligand(batch, conf_a: np.ndarray, conf_b: np.ndarray) -> np.ndarray:
+    """heavy_atom_rmsd (transform.cpp:99-113): in-frame, no superposition."""
+    ao = batch.atom_offset
+    heavy = np.concatenate([l.is_heavy.astype(bool) for l in batch.ligands])
+    d2 = np.sum((np.asarray(conf_a, np.float64) - np.asarray(conf_b, np.float64)) ** 2, axis=1)
+    out = np.zeros(batch.n_ligands)
+    for i in range(batch.n_ligands):
+        h = heavy[ao[i]:ao[i + 1]]
+        out[i] = math.sqrt(float(np.mean(d2[ao[i]:ao[i + 1]][h]))) if h.any() else 0.0
+    return out
+
+
+def topk_identical_up_to_ties(smiles, score_a, score_b, k: int) -> tuple[bool, int]:
+    """north_star: identical top-K ranking up to score ties within tolerance.
+    Rows are ranked as cmd_merge does (printed 4-decimal score desc, SMILES
+    asc; merge.cpp:131-135 via ranking.row_key).  Ligands whose printed score
+    differs between the two runs (each within the score tolerance, checked
+    separately) may move; after removing them from both rankings the first
+    k - |moved| rows must be the same sequence.  Returns (ok, |moved|)."""
+    from paper_2110_11644_b200 import ranking
+    ka = [ranking.row_key(float(s), m) for s, m in zip(score_a, smiles)]
+    kb = [ranking.row_key(float(s), m) for s, m in zip(score_b, smiles)]
+    moved = {i for i in range(len(smiles)) if ka[i] != kb[i]}
+    sk = lambda r: (-r[0], r[1].encode())  # noqa: E731
+    oa = [i for i in sorted(range(len(smiles)), key=lambda i: sk(ka[i])) if i not in moved]
+    ob = [i for i in sorted(range(len(smiles)), key=lambda i: sk(kb[i])) if i not in moved]
+    kk = max(k - len(moved), 0)
+    return oa[:kk] == ob[:kk], len(moved)
+
+
+def golden_parity(g, batch, results, conf, k_top: int = 100) -> dict:
+    """The north_star parity metrics of one run against a reference fixture."""
+    from paper_2110_11644_b200 import ranking  # noqa: F401
+    smi = [str(s) for s in g["smiles"]]
+    rel = rel_err(results["best_score"], g["best_score"])
+    rms = heavy_rmsd_per_ligand(batch, conf, g["best_conf"])
+    top_ok, moved = topk_identical_up_to_ties(smi, results["best_score"], g["best_score"], k_top)
+    return {
+        "ligands": len(smi),
+        "status_equal": float(np.mean(results["status"] == g["status"])),
+        "score_within_1e-3": float(np.mean(rel <= 1e-3)),
+        "rmsd_le_0.1": float(np.mean(rms <= 0.1)),
+        "bit_exact_score": float(np.mean(results["best_score"] == g["best_score"])),
+        "evals_equal": float(np.mean(results["scoring_evals"] == g["scoring_evals"])),
+        "topk_identical_up_to_ties": bool(top_ok), "topk_moved_rows": int(moved), "k": k_top,
+        "max_rel_err": float(np.max(rel)), "max_rmsd": float(np.max(rms)),
+    }
+
+
+def assert_north_star(rep: dict):
+    assert rep["status_equal"] == 1.0, rep
+    assert rep["score_within_1e-3"] >= 0.999, rep
+    assert rep["rmsd_le_0.1"] >= 0.999, rep
+    assert rep["evals_equal"] >= 0.999, rep
+    assert rep["topk_identical_up_to_ties"], rep
