@@ -97,8 +97,10 @@ struct vs_pocket {
   double spacing = 0.5;
   int dims[3] = {0, 0, 0};
   int n_protein = 0;
-  DevBuf values, pxyz, pclass, cell_start, cell_atoms, packed, palette;
+  DevBuf values, pxyz, pclass, cell_start, cell_atoms, packed, palette, screen;
   int packed_mode = 0;
+  bool has_screen = false;
+  vsd::screen_grid scr{};
   int bricks[2] = {0, 0};
   double cmin[3] = {0, 0, 0};
   double cs = 2.0;
@@ -137,6 +139,11 @@ struct vs_pocket {
     p.packed.c4 = packed_mode == 2 ? packed.as<uint32_t>() : nullptr;
     p.packed.inv_h = 1.0 / spacing;  // correctly rounded reciprocal for div_h
     p.palette = palette.as<double>();
+    p.scr = scr;
+    // The FP32 screen is exact but measured slower than the FP64 search on
+    // configs[1]: opt-in with VS_SCREEN=1.
+    const char *scr_env = std::getenv("VS_SCREEN");
+    p.scr.w = has_screen && scr_env && std::atoi(scr_env) != 0 ? screen.as<uint32_t>() : nullptr;
     return p;
   }
 };
@@ -226,10 +233,79 @@ vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
   return VS_OK;
 }
 
+// Screen grid of the FP32 search screen (kernels.cuh screen_grid): per cell
+// the pair-table offsets of its four x-pairs and the NU flag, plus the
+// pocket's error-model constants.  `code` = 2-bit node codes, `pal` <= 4 values.
+vs_status build_screen(vs_pocket *p, const std::vector<uint8_t> &code, const std::vector<double> &pal) {
+  const int D0 = p->dims[0], D1 = p->dims[1], D2 = p->dims[2];
+  vsd::screen_grid &s = p->scr;
+  s = vsd::screen_grid{};
+  double vmin = 0.0, vmax = 0.0, vabs = 10.0, jump = 0.0;
+  bool exact = true;
+  for (size_t c = 0; c < pal.size(); ++c) {
+    vmin = c == 0 ? pal[c] : std::min(vmin, pal[c]);
+    vmax = c == 0 ? pal[c] : std::max(vmax, pal[c]);
+    vabs = std::max(vabs, std::fabs(pal[c]));
+    jump = std::max(jump, std::fabs(pal[c] + 10.0));
+    exact = exact && static_cast<double>(static_cast<float>(pal[c])) == pal[c];
+    if (!std::isfinite(pal[c])) return VS_OK;  // no screen: non-finite node values
+  }
+  for (int i = 0; i < 16; ++i) {
+    const double a = pal[std::min<size_t>(i & 3, pal.size() - 1)], b = pal[std::min<size_t>(i >> 2, pal.size() - 1)];
+    s.pair[2 * i] = static_cast<float>(a);
+    s.pair[2 * i + 1] = static_cast<float>(b - a);
+  }
+  // error model (search.cu screen_sample): Lipschitz constant of the trilinear
+  // field summed over the three axes, in cell units; the FP32 lerp tree's
+  // rounding (7 u V) plus the table's (3 u V when a value is not FP32-exact),
+  // both padded; a uniform cell's FP32 value is exact iff the palette is.
+  const double u = std::ldexp(1.0, -24);
+  s.G = static_cast<float>(3.0 * (vmax - vmin) * (1.0 + 1e-6));
+  s.J = static_cast<float>(jump * (1.0 + 1e-6));
+  s.eval = static_cast<float>(12.0 * u * vabs);
+  s.uni = exact ? 0.0f : static_cast<float>(2.0 * u * vabs);
+  s.v3 = static_cast<float>(3.0 * vabs * (1.0 + 1e-6));
+  s.dx1 = static_cast<float>(D0 - 1);
+  s.dy1 = static_cast<float>(D1 - 1);
+  s.dz1 = static_cast<float>(D2 - 1);
+  s.fdx = static_cast<float>(D0);
+  s.fdxy = static_cast<float>(static_cast<double>(D0) * D1);
+  const size_t nv = static_cast<size_t>(D0) * D1 * D2;
+  std::vector<uint32_t> w(nv, 0u);
+  auto at = [&](int x, int y, int z) { return code[static_cast<size_t>(x) + static_cast<size_t>(D0) * (y + static_cast<size_t>(D1) * z)]; };
+  for (int iz = 0; iz + 1 < D2; ++iz)
+    for (int iy = 0; iy + 1 < D1; ++iy)
+      for (int ix = 0; ix + 1 < D0; ++ix) {
+        uint32_t word = 0;
+        for (int i = 0; i < 4; ++i) {
+          const int y = iy + (i & 1), z = iz + (i >> 1);
+          word |= static_cast<uint32_t>(8 * (at(ix, y, z) | (at(ix + 1, y, z) << 2))) << (8 * i);
+        }
+        const uint8_t c0 = at(ix, iy, iz);
+        bool nu = false;
+        for (int z = std::max(iz - 1, 0); z <= std::min(iz + 2, D2 - 1) && !nu; ++z)
+          for (int y = std::max(iy - 1, 0); y <= std::min(iy + 2, D1 - 1) && !nu; ++y)
+            for (int x = std::max(ix - 1, 0); x <= std::min(ix + 2, D0 - 1); ++x)
+              if (at(x, y, z) != c0) {
+                nu = true;
+                break;
+              }
+        if (nu) word |= 0x80000000u;
+        w[static_cast<size_t>(ix) + static_cast<size_t>(D0) * (iy + static_cast<size_t>(D1) * iz)] = word;
+      }
+  if (nv >= (1u << 22)) return VS_OK;  // the FP32 cell index needs M + index < 2^24: no screen
+  s.last = static_cast<uint32_t>(nv - 1);
+  CUDA_TRY(p->screen.ensure(sizeof(uint32_t) * nv));
+  CUDA_TRY(cudaMemcpy(p->screen.p, w.data(), sizeof(uint32_t) * nv, cudaMemcpyHostToDevice));
+  p->has_screen = true;
+  return VS_OK;
+}
+
 // Cell-packed palette grid for the search sampler (dmath.cuh): when the node
 // values take at most 4 (16) distinct doubles, each cell's 8 corner codes fit
 // in one 16-bit (32-bit) word.  Values are reproduced exactly via the palette.
 vs_status build_packed(vs_pocket *p, const double *values) {
+  p->has_screen = false;
   std::vector<double> pal;
   const size_t nv = static_cast<size_t>(p->dims[0]) * p->dims[1] * p->dims[2];
   std::vector<uint8_t> code(nv);
@@ -274,6 +350,10 @@ vs_status build_packed(vs_pocket *p, const double *values) {
         words[(brick << 6) | ((iz & 3) << 4) | ((iy & 3) << 2) | (ix & 3)] = w;
       }
   if (p->packed_mode == 1) {
+    {
+      const vs_status st = build_screen(p, code, pal);
+      if (st != VS_OK) return st;
+    }
     std::vector<uint16_t> w16(ncell);
     for (size_t i = 0; i < ncell; ++i) w16[i] = static_cast<uint16_t>(words[i]);
     CUDA_TRY(p->packed.ensure(sizeof(uint16_t) * ncell));
@@ -859,18 +939,20 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
       // Size buckets: ligands grouped by how many 4-warp search CTAs per SM
       // their shared-memory footprint allows, each bucket launched with its
       // own maxima so one large ligand does not shrink everyone's occupancy.
-      std::vector<std::vector<int>> buckets(5);
+      // bucket = CTAs per SM the ligand's own footprint allows (1..8+), the
+      // last bucket holds the ligands k_setup rejected (status only)
+      constexpr int kBuckets = 10;
+      std::vector<std::vector<int>> buckets(kBuckets);
+      const bool screen = pd.scr.w != nullptr && pd.packed.mode == 1;
       for (int i = 0; i < st.n; ++i) {
         const vsd::lig_meta &mt = meta[static_cast<size_t>(i)];
         if (mt.status != VS_LIG_OK) {
-          buckets[4].push_back(i);  // rejected by k_setup: the kernel only records the status
+          buckets[kBuckets - 1].push_back(i);
           continue;
         }
-        // warps per SM this ligand's footprint allows (registers cap it at 16)
-        const size_t bytes = vsd::search_smem_bytes(mt.n_atoms, mt.n_heavy, mt.m, mt.d_total) + 1024;
+        const size_t bytes = vsd::search_smem_bytes(mt.n_atoms, mt.n_heavy, mt.m, mt.d_total, screen) + 1024;
         const int ctas = static_cast<int>((228 * 1024) / std::max<size_t>(bytes, 1));
-        const int warps = std::min(16, ctas * vsd::search_warps_per_cta());
-        buckets[warps >= 16 ? 3 : (warps >= 12 ? 2 : (warps >= 8 ? 1 : 0))].push_back(i);
+        buckets[std::max(0, std::min(ctas, 8) - 1)].push_back(i);
       }
       std::vector<int> order;
       std::vector<std::pair<int, int>> ranges;

@@ -50,8 +50,29 @@ struct batch_dev {
   uint32_t *titems;        // 2*ditem_base[l] + ...: torsion-neighbour items h | (2t+s) << 8 | pd << 14
 };
 
+// FP32 screen of the search (search.cu): one 32-bit word per
+// cell at node index ix + dx * (iy + dy * iz); byte i (x-pair i = corners
+// (2i, 2i + 1), i.e. (y, z) = (i & 1, i >> 1)) holds 8 * (c0 | c1 << 2), the
+// offset of that pair's (a, b - a) float2 in the pair table; bit 31 = NU: the
+// 4x4x4 nodes around the cell are not all equal (a point within the screen's
+// error bound of one in a !NU cell has exactly the cell's constant value).
+// Only for pockets with <= 4 distinct node values (2-bit codes).
+struct screen_grid {
+  const uint32_t *__restrict__ w;  // NULL: no screen (the search runs in FP64 only)
+  float pair[32];                  // 16 x (a, b - a), FP32
+  float G;                         // Lipschitz bound, sum over axes, per cell unit: 3 (vmax - vmin)
+  float J;                         // largest jump at a box face: max |v - (-10)|
+  float eval;                      // FP32 interpolation error bound (NU cells)
+  float uni;                       // error of a uniform cell's FP32 value (0 when the palette is FP32-exact)
+  float v3;                        // 3 max |value|: per-item conversion errors of the row sums, / u
+  float dx1, dy1, dz1;             // dims - 1
+  float fdx, fdxy;                 // node strides dx, dx * dy (linear cell index, exact in FP32)
+  uint32_t last;                   // largest valid word index
+};
+
 struct pocket_dev {
   grid_view g;
+  screen_grid scr;
   packed_grid packed;       // cell-packed palette codes for the search sampler
   const double *palette;    // 16 values (device)
   double center[3];
@@ -125,7 +146,7 @@ cudaError_t launch_compact_right(const uint16_t *slots, const int64_t *rs_off, c
                                  int n_tors, uint16_t *right_atoms, cudaStream_t s);
 size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms);
 // dynamic shared memory of one k_search CTA for the given ligand maxima
-size_t search_smem_bytes(int N, int n, int m, int dtot);
+size_t search_smem_bytes(int N, int n, int m, int dtot, bool screen);
 int search_warps_per_cta();
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s);

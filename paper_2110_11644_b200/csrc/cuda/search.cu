@@ -132,10 +132,10 @@ __constant__ double c_lattice_lo_s[72];  // lo parts of the double-double lattic
 // Development-only phase profile (build with -DVS_PHASE_PROF): per-warp
 // clock64() time spent in each phase of the search, summed over warps.
 #ifdef VS_PHASE_PROF
-__device__ unsigned long long g_phase[16];
+__device__ unsigned long long g_phase[24];
 #define PH_DECL                        \
   unsigned long long ph_t = clock64(); \
-  unsigned long long ph_acc[16] = {0};
+  unsigned long long ph_acc[24] = {0};
 #define PH(k)                                 \
   {                                           \
     __syncwarp();                             \
@@ -145,7 +145,7 @@ __device__ unsigned long long g_phase[16];
   }
 #define PH_FLUSH \
   if (lane == 0) \
-    for (int i = 0; i < 16; ++i) atomicAdd(&g_phase[i], ph_acc[i]);
+    for (int i = 0; i < 24; ++i) atomicAdd(&g_phase[i], ph_acc[i]);
 #else
 #define PH_DECL
 #define PH(k)
@@ -163,7 +163,8 @@ enum {
   S_STEPR = 22,
   S_STEPQ = 23,
   S_ERR = 24,
-  S_N = 25
+  S_X = 25,     // screen: max |coordinate| of the heavy atoms' FP32 torsioned frame
+  S_N = 26
 };
 
 }  // namespace
@@ -187,6 +188,11 @@ struct search_args {
   int warp_doubles;
   int cta_doubles;       // CTA-shared ligand staging (after the palette)
   int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_cache, o_ang, o_sccur, o_state, o_ints;
+  // FP32 screen (SCR): heavy frame, torsion-neighbour matrices + their error
+  // constants, the 13 rigid maps (12 neighbours + current pose), the exact
+  // candidate row, FP32 current samples, FP32 stage-t prefixes
+  int o_t32, o_M32, o_kap, o_A32, o_vex, o_vc32, o_pc32;
+  size_t scr_stride;     // doubles of global scratch per warp
 };
 
 // Offset (in doubles) of variant v's matrix for torsion u >= t(v) inside the
@@ -299,7 +305,7 @@ __device__ __noinline__ void hydrogen_frame(double *hx, int N, const double *bas
 // is the same for (t,+) and (t,-) and for every step level), pairs from
 // `pfrom` on.  Recomputed only when a torsion move changes Mcur.
 __device__ __noinline__ void prefix_frame(double *pc, const uint32_t *tit, int pfrom, int npairs, const double *bh,
-                                          const uint32_t *tmh, const double *Mcur, int lane) {
+                                          const uint32_t *tmh, const double *Mcur, int lane, float *pc32 = nullptr) {
   #pragma unroll 1
   for (int p = pfrom + lane; p < npairs; p += 32) {
     const uint32_t e = tit[p];
@@ -309,7 +315,99 @@ __device__ __noinline__ void prefix_frame(double *pc, const uint32_t *tit, int p
     for (uint32_t bb = tmh[h] & ((1u << t) - 1u); bb; bb &= bb - 1u)
       x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
     st3(pc + 3 * p, x);
+    if (pc32) {
+      pc32[3 * p] = (float)x.x;
+      pc32[3 * p + 1] = (float)x.y;
+      pc32[3 * p + 2] = (float)x.z;
+    }
   }
+}
+
+// ---------------------------------------------------------------------------
+// FP32 screen.  Every neighbour's geo_score is first
+// bracketed in FP32 with a proven error bound; only the neighbours whose
+// bracket reaches the decision threshold are evaluated exactly in FP64 (the
+// reference's arithmetic, unchanged), so the adopted neighbour -- and every
+// bit of the trajectory -- is the reference's.
+//
+// Error model (u = 2^-24; vectors in the 2-norm unless marked inf):
+//  * rigid map l = A x + b (A = fl32(R / h), b = fl32((t - o) / h), x =
+//    fl32(frame)), three FMAs per axis: |l~ - l| <= u (5.01 sqrt3 X / h +
+//    4.01 |b|inf) per axis (X = |x|inf bound), padded to 5.1 / 4.1; the
+//    reference's own FP64 rounding (<1e-13 cells) is covered by +1e-9;
+//  * torsion chain y = R (x - p) + p in FP32 per applied matrix: the error
+//    grows by sqrt3 u (7.94 |d|inf + 5.01 |p|inf) (padded to 8.7 / 5.75) and
+//    is carried through rotations unamplified; the prefix's own rounding adds
+//    sqrt3 u |x|inf; the rigid map then scales it by 1 / h;
+//  * sample: trilinear interpolation is Lipschitz with sum-over-axes constant
+//    G = 3 (vmax - vmin) per cell unit, so |f(l~) - f(l)| <= G dl; FP32
+//    lerp rounding <= 7 u V (+ table rounding) = `eval`; in a cell whose 4^3
+//    node neighbourhood is uniform (!NU) the value is exactly the constant;
+//    within dl of a box face the -10 jump J is added;
+//  * row: s~ = fl32(S) + sum (v~ - fl32(vcur)) over the moved atoms (the
+//    others sample exactly as the current pose), FP32 summation error
+//    <= (k + 2) u (|S| + sum |d|), per-item conversions <= 3 u V; the
+//    reference's two FP64 sums differ from the real ones by < 1e-11.
+// ---------------------------------------------------------------------------
+constexpr float kU32 = 5.9604645e-8f;  // 2^-24
+constexpr float kSqrt3 = 1.7320508f;
+
+__device__ __forceinline__ float screen_sample(const screen_grid &sg, const float *tab, float lx, float ly, float lz,
+                                               float dl, float &e) {
+  constexpr float M = 12582912.0f;  // 1.5 * 2^23: fadd.rm gives M + floor(l) for |l| < 2^22
+  const float tx = __fadd_rd(lx, M), ty = __fadd_rd(ly, M), tz = __fadd_rd(lz, M);
+  const float flx = tx - M, fly = ty - M, flz = tz - M;
+  const float fx = lx - flx, fy = ly - fly, fz = lz - flz;  // exact for l >= 0
+  // linear cell index ix + dx (iy + dy iz), exact while M + index < 2^24;
+  // out-of-box points are clamped into the array and overridden below
+  const float fi = fmaf(flz, sg.fdxy, fmaf(fly, sg.fdx, tx));
+  const uint32_t idx = min((uint32_t)(__float_as_int(fi) - 0x4B400000), sg.last);
+  const uint32_t w = __ldg(sg.w + idx);
+  const char *tb = reinterpret_cast<const char *>(tab);
+  const float2 c0 = *reinterpret_cast<const float2 *>(tb + (w & 0xffu));
+  const float2 c1 = *reinterpret_cast<const float2 *>(tb + ((w >> 8) & 0xffu));
+  const float2 c2 = *reinterpret_cast<const float2 *>(tb + ((w >> 16) & 0xffu));
+  const float2 c3 = *reinterpret_cast<const float2 *>(tb + ((w >> 24) & 0x7fu));
+  const float X0 = fmaf(fx, c0.y, c0.x), X1 = fmaf(fx, c1.y, c1.x);
+  const float X2 = fmaf(fx, c2.y, c2.x), X3 = fmaf(fx, c3.y, c3.x);
+  const float Y0 = fmaf(fy, X1 - X0, X0), Y1 = fmaf(fy, X3 - X2, X2);
+  float v = fmaf(fz, Y1 - Y0, Y0);
+  // signed distance to the nearest node-box face (inf-norm, > 0 inside);
+  // l - (dims - 1) is exact near the face (Sterbenz)
+  const float lo = fminf(fminf(lx, ly), lz);
+  const float hi = fmaxf(fmaxf(lx - sg.dx1, ly - sg.dy1), lz - sg.dz1);
+  const float mg = fminf(lo, -hi);
+  const float g = fmaf(sg.G, dl, sg.eval);
+  float ee = (int)w < 0 ? g : sg.uni;
+  ee = mg <= dl ? sg.J + g : ee;  // within dl of a face: either side
+  const bool out = mg < -dl;      // outside for the reference too: exactly -10
+  e = out ? 0.0f : ee;
+  return out ? -10.0f : v;
+}
+
+// One FP32 rigid map slot (16 floats): A = R / h (9), b = (t - o) / h (3),
+// the per-axis bound dl of a rigid item whose frame |x|inf <= X, |b|inf.
+__device__ __forceinline__ void screen_slot(const double *R, const double *T, const grid_view &g, double inv_h,
+                                            double X, float *out) {
+  #pragma unroll 1
+  for (int i = 0; i < 9; ++i) out[i] = (float)(R[i] * inv_h);
+  out[9] = (float)((T[0] - g.ox) * inv_h);
+  out[10] = (float)((T[1] - g.oy) * inv_h);
+  out[11] = (float)((T[2] - g.oz) * inv_h);
+  const float B = fmaxf(fmaxf(fabsf(out[9]), fabsf(out[10])), fabsf(out[11]));
+  const float base = kU32 * 4.1f * B + 1e-9f;
+  out[12] = fmaf(kU32 * 5.1f * kSqrt3 * (float)inv_h * 1.0001f, (float)X * 1.0001f, base);
+  out[13] = base;  // torsion items add their own frame term
+}
+
+__device__ __forceinline__ void screen_map(const float *S, float x0, float x1, float x2, float &lx, float &ly,
+                                           float &lz) {
+  const float4 a0 = *reinterpret_cast<const float4 *>(S);
+  const float4 a1 = *reinterpret_cast<const float4 *>(S + 4);
+  const float4 a2 = *reinterpret_cast<const float4 *>(S + 8);
+  lx = fmaf(a0.z, x2, fmaf(a0.y, x1, fmaf(a0.x, x0, a2.y)));
+  ly = fmaf(a1.y, x2, fmaf(a1.x, x1, fmaf(a0.w, x0, a2.z)));
+  lz = fmaf(a2.x, x2, fmaf(a1.w, x1, fmaf(a1.z, x0, a2.w)));
 }
 
 // The whole conformation of the current pose into `out` (3N, atom order):
@@ -341,12 +439,28 @@ __device__ __forceinline__ void compute_pivot(double *scratch, double *S, int N,
   __syncwarp();
 }
 
-template <int MODE>
+__device__ __forceinline__ float frame_max32(const float *t32, int n, int lane) {
+  float x = 0.0f;
+  #pragma unroll 1
+  for (int i = lane; i < 3 * n; i += 32) x = fmaxf(x, fabsf(t32[i]));
+  #pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, off));
+  return x;
+}
+
 #ifndef VS_SEARCH_MINB
 #define VS_SEARCH_MINB (16 / kWarps)  // A/B only: a higher count caps the registers (96 at 10: +9% search time)
 #endif
-__global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_args A) {
+#ifndef VS_SCREEN_MINB
+#define VS_SCREEN_MINB 7
+#endif
+constexpr int kMaxWarpsSM = 24;  // warp slots per SM in the global scratch
+
+template <int MODE, bool SCR>
+__global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_MINB) k_search(search_args A) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(16) float s_pair[32];  // screen pair table: 16 x (a, b - a)
+  if (SCR && threadIdx.x < 32) s_pair[threadIdx.x] = A.p.scr.pair[threadIdx.x];
   // palette (CTA-wide): MODE 2 reads the 16 values; MODE 1 a table of code
   // pairs, entry i = (palette[i & 3], palette[i >> 2]), so two corners of a
   // cell come with one 128-bit load
@@ -375,15 +489,28 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
 #endif
   // per-warp global scratch: the hydrogens' torsioned frame (3 * Nmax) and
   // the stage-t prefix positions of the torsion items (3 * nmax * mmax)
-  double *hx = A.hscr + (size_t)(blockIdx.x * kWarps + warp) * 3 * (A.Nmax + A.nmax * A.mmax);
+  double *hx = A.hscr + (size_t)(blockIdx.x * kWarps + warp) * A.scr_stride;
   double *pc = hx + 3 * A.Nmax;
   // per-CTA global slot (dock path): the start matrices of flatten's angles
   // and their sin/cos, computed once per ligand for all its restarts
-  double *M0 = A.hscr + (size_t)A.scr_warps * 3 * (A.Nmax + A.nmax * A.mmax) + (size_t)blockIdx.x * 14 * A.mmax;
+  double *M0 = A.hscr + (size_t)A.scr_warps * A.scr_stride + (size_t)blockIdx.x * 14 * A.mmax;
   double *sc0 = M0 + 12 * A.mmax;
   VS_CHECK((int)(blockIdx.x * kWarps + warp) < A.scr_warps);
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
+  float *t32 = reinterpret_cast<float *>(W + A.o_t32);
+  float *M32 = reinterpret_cast<float *>(W + A.o_M32);
+  float *kap = reinterpret_cast<float *>(W + A.o_kap);
+  float *A32 = reinterpret_cast<float *>(W + A.o_A32);
+  float *vc32 = reinterpret_cast<float *>(W + A.o_vc32);
+  // screen: FP32 stage-t prefixes in the warp's global scratch (read in the
+  // torsion screen, rewritten only after a torsion move)
+  float *pc32 = reinterpret_cast<float *>(hx + ((3 * (size_t)A.Nmax + 3 * (size_t)A.nmax * A.mmax + 1) & ~(size_t)1));
+  int *crow = reinterpret_cast<int *>(W + A.o_pc32);  // screen: candidate rows and item ends of a batch
+  float *s_ub = reinterpret_cast<float *>(W + A.o_vex);  // screen: upper bound of every neighbour row
+  const screen_grid &sg = A.p.scr;
+  float Xf = 0.0f;  // screen: |frame|inf bound of the rigid items
+  unsigned mgn = 1u;  // screen: ceil(2^32 / n), it / n == umulhi(it, mgn) for the rigid items
   double *Rj = W + A.o_Rj;       // 6 spin neighbours x kRow: R at 0, t at 10, q at 14 (16-byte aligned)
   double *Tj = Rj + 6 * kRow;    // 6 translation neighbours' t, stride 4
   double *vb = W + A.o_vb;
@@ -423,6 +550,7 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
       continue;
     }
     const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
+    if (SCR) mgn = n > 1 ? (unsigned)(0xffffffffu / (unsigned)n) + 1u : 1u;
     const int a0 = b.atom_off[l], t0 = b.tors_off[l];
     const double *base = b.xyz + 3 * (size_t)a0;
     const uint32_t *tm = b.atom_tmask + a0;
@@ -511,9 +639,20 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
       #pragma unroll 1
       for (int i = lane; i < 3 * N; i += 32) hx[i] = A.f.xyz[3 * (size_t)a0 + i];
 #if VS_TORSH_SMEM
-      #pragma unroll 1
-      for (int h = lane; h < n; h += 32) st3(torsh + 3 * h, ld3(A.f.xyz + 3 * ((size_t)a0 + s_hl[h])));
+      if (!SCR) {
+        #pragma unroll 1
+        for (int h = lane; h < n; h += 32) st3(torsh + 3 * h, ld3(A.f.xyz + 3 * ((size_t)a0 + s_hl[h])));
+      }
 #endif
+      if (SCR) {
+        #pragma unroll 1
+        for (int h = lane; h < n; h += 32) {
+          const d3 x = ld3(A.f.xyz + 3 * ((size_t)a0 + s_hl[h]));
+          t32[3 * h] = (float)x.x;
+          t32[3 * h + 1] = (float)x.y;
+          t32[3 * h + 2] = (float)x.z;
+        }
+      }
     } else {
       if (lane == 0 && m > 0 && !chain_mats(0, sccur[0], sccur[1], m, s_ep, s_epm, Mcur, sccur, Mcur))
         S[S_ERR] = 1.0;
@@ -530,15 +669,21 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
         for (uint32_t bb = s_tmh[h] & 0x7fffffffu; bb; bb &= bb - 1u)
           x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
 #if VS_TORSH_SMEM
-        st3(torsh + 3 * h, x);
+        if (!SCR) st3(torsh + 3 * h, x);
 #endif
+        if (SCR) {
+          t32[3 * h] = (float)x.x;
+          t32[3 * h + 1] = (float)x.y;
+          t32[3 * h + 2] = (float)x.z;
+        }
         st3(hx + 3 * s_hl[h], x);  // every atom's frame also in hx (pivots, outputs)
       }
       hydrogen_frame(hx, N, base, tm, hv, Mcur, 0xffffffffu, lane);
     }
     __syncwarp();
-    prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane);
+    prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane, SCR ? pc32 : nullptr);
     __syncwarp();
+    if (SCR) Xf = frame_max32(t32, n, lane);
     // initial_poses entry point: the flat centroid of these angles
     // (search.cpp:89-90) instead of flatten's
     if (!ls_mode && A.ang_in) {
@@ -580,7 +725,9 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
     for (int h = lane; h < n; h += 32) {
       const int a = s_hl[h];
       bool out;
-      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(S + S_R, S + S_T, ld3(TORSH(h, a)), a), out);
+      vcur[h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(S + S_R, S + S_T, ld3(SCR ? hx + 3 * a : TORSH(h, a)), a),
+                                       out);
+      if (SCR) vc32[h] = (float)vcur[h];
     }
     __syncwarp();
     if (lane == 0) {
@@ -646,6 +793,16 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
           X[17] = qn.w;
         }
       }
+      if (SCR) {
+        __syncwarp();
+        // FP32 maps of the 12 rigid neighbours (slots 0-11) and the current
+        // pose (slot 12, torsion neighbours)
+        if (lane < 13) {
+          const double *R = (lane < 6 || lane == 12) ? S + S_R : Rj + kRow * (lane - 6);
+          const double *T = lane < 6 ? Tj + 4 * lane : (lane == 12 ? S + S_T : R + 10);
+          screen_slot(R, T, g, pg.inv_h, Xf, A32 + 16 * lane);
+        }
+      }
 #ifdef VS_PHASE_PROF
       __syncwarp();
       pr_rg = (unsigned int)(clock64() - pr0);
@@ -698,6 +855,18 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
         ph_acc[14] += pr_rg;
       }
 #endif
+      if (SCR && !mvar_valid) {
+        // the screen's FP32 copies of the torsion-neighbour matrices (all
+        // lanes, coalesced) and their error constants 5.75 |p~|inf
+        __syncwarp();
+        const int nm12 = 12 * m * (m + 1);
+        #pragma unroll 1
+        for (int i = lane; i < nm12; i += 32) M32[i] = (float)Mvar[i];
+        __syncwarp();
+        #pragma unroll 1
+        for (int i = lane; i < m * (m + 1); i += 32)
+          kap[i] = 5.75f * fmaxf(fmaxf(fabsf(M32[12 * i + 9]), fabsf(M32[12 * i + 10])), fabsf(M32[12 * i + 11]));
+      }
       mvar_valid = true;
       __syncwarp();
       PH(ph_rebuild ? 9 : 1)
@@ -713,6 +882,8 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
       double bv = S[S_GEO];
       int bj = -1;
       int tg = 0;  // next torsion to schedule
+      float lbmax = -__int_as_float(0x7f800000);  // screen: largest proven lower bound so far
+      const float S32 = (float)bv, aS = fabsf(S32);
       for (int grp = 0; grp == 0 || tg < m; ++grp) {
         int j0, jn, tlo = 0, thi = 0, items;
         if (grp == 0) {
@@ -726,6 +897,108 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
           j0 = 12 + 2 * tlo;
           jn = 2 * (thi - tlo);
           items = 2 * (s_doff[thi - 1] + s_dcnt[thi - 1] - s_doff[tlo]);
+        }
+        if constexpr (SCR) {
+          // ---- FP32 screen of the group: per item (v~ - fl32(vcur), bound).
+          // One loop and one sampler call site for both neighbour kinds (the
+          // search is instruction-cache bound: the hot code must stay small).
+          float2 *vs2 = reinterpret_cast<float2 *>(vb);
+          {
+            const bool rig = grp == 0;
+            const uint32_t *ti = s_tit + s_doff[tlo];
+            const float *pcg = pc32 + 3 * s_doff[tlo];
+            const float cY = kU32 * 5.1f * kSqrt3 * (float)pg.inv_h * 1.0001f;
+            const float cE = kU32 * kSqrt3 * 1.01f * (float)pg.inv_h;
+            #pragma unroll 1
+            for (int it = lane; it < items; it += 32) {
+              const float *Sj;
+              float x0, x1, x2, eacc = 0.0f;
+              int h;
+              if (rig) {
+                const int j = n == 1 ? it : (int)__umulhi((unsigned)it, mgn);
+                h = it - j * n;
+                Sj = A32 + 16 * j;
+                x0 = t32[3 * h];
+                x1 = t32[3 * h + 1];
+                x2 = t32[3 * h + 2];
+              } else {
+                // torsion item: pair (t, h in D_t) it / 2, sign it & 1, from its
+                // FP32 stage-t prefix through the variant's FP32 matrices
+                const uint32_t e = ti[it >> 1];
+                const int v = ((e >> 8) & 63) | (it & 1), t = v >> 1;
+                h = e & 255;
+                x0 = pcg[3 * (it >> 1)];
+                x1 = pcg[3 * (it >> 1) + 1];
+                x2 = pcg[3 * (it >> 1) + 2];
+                eacc = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fabsf(x2));
+                const int mb = mvar_off(v, t, m) / 12 - t;
+                #pragma unroll 1
+                for (uint32_t bb = (s_tmh[h] & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u) {
+                  const int mi = mb + __ffs(bb) - 1;
+                  const float4 q0 = *reinterpret_cast<const float4 *>(M32 + 12 * mi);
+                  const float4 q1 = *reinterpret_cast<const float4 *>(M32 + 12 * mi + 4);
+                  const float4 q2 = *reinterpret_cast<const float4 *>(M32 + 12 * mi + 8);
+                  const float d0 = x0 - q2.y, d1 = x1 - q2.z, d2 = x2 - q2.w;
+                  const float D = fmaxf(fmaxf(fabsf(d0), fabsf(d1)), fabsf(d2));
+                  x0 = fmaf(q0.z, d2, fmaf(q0.y, d1, fmaf(q0.x, d0, q2.y)));
+                  x1 = fmaf(q1.y, d2, fmaf(q1.x, d1, fmaf(q0.w, d0, q2.z)));
+                  x2 = fmaf(q2.x, d2, fmaf(q1.w, d1, fmaf(q1.z, d0, q2.w)));
+                  eacc += fmaf(8.7f, D, kap[mi]);
+                }
+                Sj = A32 + 16 * 12;
+              }
+              float lx, ly, lz;
+              screen_map(Sj, x0, x1, x2, lx, ly, lz);
+              const float Y = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fabsf(x2));
+              const float dl = rig ? Sj[12] : fmaf(cE, eacc, fmaf(cY, Y, Sj[13]));
+              float e;
+              const float val = screen_sample(sg, s_pair, lx, ly, lz, dl, e);
+              vs2[it] = make_float2(val - vc32[h], e);
+            }
+          }
+          __syncwarp();
+          PH(grp == 0 ? 2 : 3)
+          // ---- per-row bracket [lb, ub] of the exact geo_score
+          float ub = -__int_as_float(0x7f800000), lb = ub;
+          if (lane < jn) {
+            int base, k, stride;
+            if (grp == 0) {
+              base = lane * n;
+              k = n;
+              stride = 1;
+            } else {
+              const int t = tlo + (lane >> 1);
+              base = 2 * (s_doff[t] - s_doff[tlo]) + (lane & 1);
+              k = s_dcnt[t];
+              stride = 2;
+            }
+            float sd = 0.0f, sa = 0.0f, se = 0.0f;
+            #pragma unroll 4
+            for (int i = 0; i < k; ++i) {
+              const float2 q = vs2[base + i * stride];
+              sd += q.x;
+              sa += fabsf(q.x);
+              se += q.y;
+            }
+            const float st = S32 + sd;
+            const float E = fmaf(kU32, fmaf((float)(k + 2), aS + sa, sg.v3 * (float)k), se + 1e-9f) * 1.001f;
+            ub = __fadd_ru(st, E);
+            lb = __fadd_rd(st, -E);
+            if (isnan(ub) || isnan(lb)) {  // non-finite inputs: evaluate exactly (the reference never adopts NaN)
+              ub = __int_as_float(0x7f800000);
+              lb = -ub;
+            }
+          }
+#ifdef VS_PHASE_PROF
+          ph_acc[17] += jn;
+#endif
+          float gl = lb;
+          #pragma unroll
+          for (int off = 16; off > 0; off >>= 1) gl = fmaxf(gl, __shfl_xor_sync(0xffffffffu, gl, off));
+          lbmax = fmaxf(lbmax, gl);
+          if (lane < jn) s_ub[j0 + lane] = ub;
+          __syncwarp();
+          continue;
         }
         // Rigid and torsion neighbours run in separate compact loops, one
         // sample in flight per lane: the search is instruction-fetch bound
@@ -854,6 +1127,120 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
         __syncwarp();
         PH(4)
       }
+      if constexpr (SCR) {
+        // ---- exact FP64 evaluation of every neighbour whose bracket reaches
+        // tau = max(current score, largest lower bound): in neighbour order,
+        // batches of <= kGroup rows in one flattened pass (rows into vb)
+        const double tau = fmax(bv, (double)lbmax);
+        #pragma unroll 1
+        for (int J0 = 0; J0 < J; J0 += 32) {
+          unsigned cand = __ballot_sync(0xffffffffu, J0 + lane < J && (double)s_ub[J0 + lane] >= tau);
+          #pragma unroll 1
+          while (cand) {
+            unsigned batch = cand;
+            if (__popc(batch) > kGroup) batch &= (1u << (__fns(batch, 0, kGroup + 1))) - 1u;
+            cand &= ~batch;
+            const int K = __popc(batch);
+            int cnt = 0;
+            if ((batch >> lane) & 1u) {
+              const int ci = __popc(batch & ((1u << lane) - 1u));
+              const int row = J0 + lane;
+              crow[ci] = row;
+              cnt = row < 12 ? n : s_dcnt[(row - 12) >> 1];
+            }
+            int incl = cnt;  // inclusive scan of the item counts in row order
+            #pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const int o = __shfl_up_sync(0xffffffffu, incl, off);
+              if (lane >= off) incl += o;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if ((batch >> lane) & 1u) crow[kGroup + __popc(batch & ((1u << lane) - 1u))] = incl;
+            __syncwarp();
+#ifdef VS_PHASE_PROF
+            ph_acc[16] += K;
+#endif
+            double *vx = vb;  // K rows of nmax doubles
+            #pragma unroll 1
+            for (int it = lane; it < total; it += 32) {
+              int ci = 0, first = 0;
+              #pragma unroll 1
+              for (int c = 0; c < K; ++c) {
+                const int end = crow[kGroup + c];
+                if (it < end) {
+                  ci = c;
+                  break;
+                }
+                first = end;
+              }
+              const int row = crow[ci], i = it - first;
+              const double *R = S + S_R, *T = S + S_T;
+              int h, col;
+              d3 x;
+              if (row < 12) {
+                if (row >= 6) {
+                  R = Rj + kRow * (row - 6);
+                  T = R + 10;
+                } else {
+                  T = Tj + 4 * row;
+                }
+                h = i;
+                col = s_hl[i];
+                x = ld3(hx + 3 * col);
+              } else {
+                const int v = row - 12, t = v >> 1;
+                const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;
+                const int pp = s_doff[t] + i;
+                h = s_tit[pp] & 255;
+                x = ld3(pc + 3 * pp);
+                const uint32_t mask = s_tmh[h];
+                col = (int)(mask >> 31);
+                #pragma unroll 1
+                for (uint32_t bb = (mask & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u)
+                  x = torsion_apply_a(Mv + 12 * (__ffs(bb) - 1), x);
+              }
+              bool out;
+              vx[ci * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, col), out);
+            }
+            __syncwarp();
+            // geo_score of each candidate: the reference's sequential sum in
+            // heavy-atom order (grid.cpp:97-101), atoms outside D_t from the
+            // current pose; then the first strict maximum (search.cpp:138)
+            double acc = -__longlong_as_double(0x7ff0000000000000LL);
+            int rr = 0x7fffffff, ci = lane;
+            if (lane < K) {
+              rr = crow[lane];
+              const double *rw = vx + lane * nmax;
+              const uint32_t tb = rr < 12 ? 0xffffffffu : 1u << ((rr - 12) >> 1);
+              double a = 0.0;
+              #pragma unroll 4
+              for (int h = 0; h < n; ++h) a += (rr < 12 || (s_dm[h] & tb)) ? rw[h] : vcur[h];
+              acc = isnan(a) ? acc : a;
+            }
+            #pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, acc, off);
+              const int orr = __shfl_xor_sync(0xffffffffu, rr, off);
+              const int oci = __shfl_xor_sync(0xffffffffu, ci, off);
+              if (ov > acc || (ov == acc && orr < rr)) {
+                acc = ov;
+                rr = orr;
+                ci = oci;
+              }
+            }
+            if (acc > bv) {
+              bv = acc;
+              bj = rr;
+              const double *rw = vx + ci * nmax;
+              const uint32_t tb = rr < 12 ? 0xffffffffu : 1u << ((rr - 12) >> 1);
+              #pragma unroll 1
+              for (int h = lane; h < n; h += 32) vbest[h] = (rr < 12 || (s_dm[h] & tb)) ? rw[h] : vcur[h];
+            }
+            __syncwarp();
+          }
+        }
+        PH(4)
+      }
       evals += (unsigned long long)n * J;
       ++n_iter;
       if (bj >= 0) {
@@ -899,15 +1286,27 @@ __global__ void __launch_bounds__(32 * kWarps, VS_SEARCH_MINB) k_search(search_a
             for (uint32_t bb = (s_tmh[h] & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u)
               x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
 #if VS_TORSH_SMEM
-            st3(torsh + 3 * h, x);
+            if (!SCR) st3(torsh + 3 * h, x);
 #endif
+            if (SCR) {
+              t32[3 * h] = (float)x.x;
+              t32[3 * h + 1] = (float)x.y;
+              t32[3 * h + 2] = (float)x.z;
+            }
             st3(hx + 3 * s_hl[h], x);
           }
           hydrogen_frame(hx, N, base, tm, hv, Mcur, dep, lane);
-          prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane);
+          prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane, SCR ? pc32 : nullptr);
+          if (SCR) {
+            __syncwarp();
+            Xf = frame_max32(t32, n, lane);
+          }
         }
         #pragma unroll 1
-        for (int h = lane; h < n; h += 32) vcur[h] = vbest[h];
+        for (int h = lane; h < n; h += 32) {
+          vcur[h] = vbest[h];
+          if (SCR) vc32[h] = (float)vbest[h];
+        }
         if (lane == 0) S[S_GEO] = bv;
         __syncwarp();
         // new pivot = centroid of the adopted conformation (vb is free here)
@@ -966,10 +1365,11 @@ namespace {
 
 struct Layout {
   int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_cache, o_ang, o_sccur, o_state, o_ints, total;
+  int o_t32, o_M32, o_kap, o_A32, o_vex, o_vc32, o_pc32;
   int cta;  // CTA-shared ligand staging, doubles
 };
 
-Layout layout(int Nm, int nm, int mm, int dm) {
+Layout layout(int Nm, int nm, int mm, int dm, bool scr) {
   Layout L{};
   L.cta = 3 * nm + 6 * mm + (3 * nm + 4 * mm + dm + 1) / 2 + 1;
   L.cta = (L.cta + 1) & ~1;
@@ -979,11 +1379,11 @@ Layout layout(int Nm, int nm, int mm, int dm) {
     o += (n + 1) & ~1;  // keep 16-byte alignment
     return at;
   };
-  L.o_tors = take(VS_TORSH_SMEM ? 3 * nm : 0);
+  L.o_tors = take(VS_TORSH_SMEM && !scr ? 3 * nm : 0);
   L.o_Mcur = take(12 * mm);
   L.o_Mvar = take(12 * mm * (mm + 1));
   L.o_Rj = take(kRow * 6 + 4 * 6);
-  L.o_vb = take(kGroup * nm > 3 * Nm ? kGroup * nm : 3 * Nm);  // also the pivot scratch
+  L.o_vb = take(kGroup * nm > 3 * Nm ? kGroup * nm : 3 * Nm);  // also the pivot scratch / screen items (float2)
   L.o_vbest = take(nm);
   L.o_vcur = take(nm);
   L.o_cache = take(8 * mm);  // sin/cos of the 2m variant angles: hi parts, then lo parts
@@ -991,12 +1391,31 @@ Layout layout(int Nm, int nm, int mm, int dm) {
   L.o_sccur = take(4 * mm);  // sin/cos of the current angles: hi parts, then lo parts
   L.o_state = take(S_N);
   L.o_ints = take((2 * mm + 1) / 2 + 1);
+  if (scr) {
+    L.o_t32 = take((3 * nm + 1) / 2);
+    L.o_M32 = take(6 * mm * (mm + 1));     // 12 floats per matrix
+    L.o_kap = take((mm * (mm + 1) + 1) / 2);
+    L.o_A32 = take(13 * 8);               // 13 slots x 16 floats
+    L.o_vex = take((12 + 2 * mm + 1) / 2);  // row upper bounds (floats)
+    L.o_vc32 = take((nm + 1) / 2);
+    L.o_pc32 = take(kGroup);  // candidate rows and their item ends (ints)
+  }
   L.total = o;
   return L;
 }
 
+// Global scratch per warp, in doubles: hydrogen frame (3 Nmax), stage-t
+// prefixes (3 nmax mmax) and their FP32 copies (screen), 16-byte aligned.
+size_t scr_stride(int Nm, int nm, int mm) {
+  const size_t pre = (3 * (size_t)Nm + 3 * (size_t)nm * mm + 1) & ~(size_t)1;
+  return pre + ((3 * (size_t)nm * mm + 3) / 2 & ~(size_t)1) + 2;
+}
+
+bool use_screen(const search_args &A) { return A.pg.mode == 1 && A.p.scr.w != nullptr; }
+
 cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launches) {
-  const Layout L = layout(A.Nmax, A.nmax, A.mmax, A.dmax);
+  const bool scr = use_screen(A);
+  const Layout L = layout(A.Nmax, A.nmax, A.mmax, A.dmax, scr);
   A.cta_doubles = L.cta;
   A.o_tors = L.o_tors;
   A.o_Mcur = L.o_Mcur;
@@ -1010,34 +1429,47 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   A.o_sccur = L.o_sccur;
   A.o_state = L.o_state;
   A.o_ints = L.o_ints;
+  A.o_t32 = L.o_t32;
+  A.o_M32 = L.o_M32;
+  A.o_kap = L.o_kap;
+  A.o_A32 = L.o_A32;
+  A.o_vex = L.o_vex;
+  A.o_vc32 = L.o_vc32;
+  A.o_pc32 = L.o_pc32;
   A.warp_doubles = L.total;
+  A.scr_stride = scr_stride(A.Nmax, A.nmax, A.mmax);
   const int o = L.total;
   const size_t smem = (size_t)(kPalDoubles + L.cta + o * kWarps) * sizeof(double);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  const void *fn = A.pg.mode == 1 ? (const void *)k_search<1>
-                                  : (A.pg.mode == 2 ? (const void *)k_search<2> : (const void *)k_search<0>);
+  if (smem > 227 * 1024 - 256) return cudaErrorInvalidValue;
+  const void *fn = scr ? (const void *)k_search<1, true>
+                       : (A.pg.mode == 1 ? (const void *)k_search<1, false>
+                                         : (A.pg.mode == 2 ? (const void *)k_search<2, false>
+                                                           : (const void *)k_search<0, false>));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
-  // the global scratch holds 16 warps per SM (search_scratch_bytes)
-  if (per_sm > 16 / kWarps) per_sm = 16 / kWarps;
+  // the global scratch holds kMaxWarpsSM warps per SM (search_scratch_bytes)
+  if (per_sm > kMaxWarpsSM / kWarps) per_sm = kMaxWarpsSM / kWarps;
 #ifdef VS_PROF_CTAS_PER_SM
   per_sm = VS_PROF_CTAS_PER_SM;  // development: phase timing without co-resident warps
 #endif
+  if (const char *cap = std::getenv("VS_SEARCH_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(cap)));
   int blocks = num_sms * per_sm;
   if (blocks > A.n_lig) blocks = A.n_lig;
   if (blocks < 1) blocks = 1;
   if (std::getenv("VSDOCK_DEBUG"))
-    std::fprintf(stderr, "k_search: %d ligands, N<=%d n<=%d m<=%d d<=%d, smem %zu B/CTA, %d CTAs/SM, %d CTAs\n", A.n_lig,
-                 A.Nmax, A.nmax, A.mmax, A.dmax, smem, per_sm, blocks);
-  if (A.pg.mode == 1)
-    k_search<1><<<blocks, 32 * kWarps, smem, s>>>(A);
+    std::fprintf(stderr, "k_search%s: %d ligands, N<=%d n<=%d m<=%d d<=%d, smem %zu B/CTA, %d CTAs/SM, %d CTAs\n",
+                 scr ? " (screen)" : "", A.n_lig, A.Nmax, A.nmax, A.mmax, A.dmax, smem, per_sm, blocks);
+  if (scr)
+    k_search<1, true><<<blocks, 32 * kWarps, smem, s>>>(A);
+  else if (A.pg.mode == 1)
+    k_search<1, false><<<blocks, 32 * kWarps, smem, s>>>(A);
   else if (A.pg.mode == 2)
-    k_search<2><<<blocks, 32 * kWarps, smem, s>>>(A);
+    k_search<2, false><<<blocks, 32 * kWarps, smem, s>>>(A);
   else
-    k_search<0><<<blocks, 32 * kWarps, smem, s>>>(A);
+    k_search<0, false><<<blocks, 32 * kWarps, smem, s>>>(A);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -1051,27 +1483,28 @@ void set_lattice_table_search(const double *sc72, const double *lo72) {
 
 #ifdef VS_PHASE_PROF
 extern "C" int vs_debug_phase_read(unsigned long long *out, int reset) {
-  cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 24);
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[24] = {0};
     cudaMemcpyToSymbol(g_phase, z, sizeof z);
   }
   return 0;
 }
 #endif
 
-// Global scratch of the search per resident warp: hydrogen frame and the
-// torsion items' prefix positions.
+// Global scratch of the search: per resident warp slot (kMaxWarpsSM per SM)
+// scr_stride doubles, then a 14 mmax-double slot per CTA.
 size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sms) {
-  const size_t N = nmax_atoms > 0 ? nmax_atoms : 1, n = nmax_heavy > 0 ? nmax_heavy : 1, m = mmax > 0 ? mmax : 1;
-  return ((size_t)num_sms * 16 * 3 * (N + n * m) + (size_t)num_sms * 16 * 14 * m) * sizeof(double);
+  const int N = nmax_atoms > 0 ? nmax_atoms : 1, n = nmax_heavy > 0 ? nmax_heavy : 1, m = mmax > 0 ? mmax : 1;
+  const size_t warps = (size_t)num_sms * kMaxWarpsSM;
+  return (warps * scr_stride(N, n, m) + warps * 14 * (size_t)m) * sizeof(double);
 }
 
 int search_warps_per_cta() { return kWarps; }
 
-size_t search_smem_bytes(int N, int n, int m, int dtot) {
-  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1, dtot > 0 ? dtot : 1);
-  return (size_t)(kPalDoubles + L.cta + L.total * kWarps) * sizeof(double);
+size_t search_smem_bytes(int N, int n, int m, int dtot, bool screen) {
+  const Layout L = layout(N > 0 ? N : 1, n > 0 ? n : 1, m > 0 ? m : 1, dtot > 0 ? dtot : 1, screen);
+  return (size_t)(kPalDoubles + L.cta + L.total * kWarps) * sizeof(double) + (screen ? 128 : 0);
 }
 
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
@@ -1080,7 +1513,7 @@ cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_
                           int n_lig, int dmax) {
   search_args A{};
   A.hscr = static_cast<double *>(args_buf);
-  A.scr_warps = num_sms * 16;
+  A.scr_warps = num_sms * kMaxWarpsSM;
   A.b = b;
   A.p = p;
   A.pg = p.packed;
@@ -1103,7 +1536,7 @@ cudaError_t launch_initial_poses(const batch_dev &b, const pocket_dev &p, const 
                                  int num_sms, cudaStream_t s, void *args_buf) {
   search_args A{};
   A.hscr = static_cast<double *>(args_buf);
-  A.scr_warps = num_sms * 16;
+  A.scr_warps = num_sms * kMaxWarpsSM;
   A.b = b;
   A.p = p;
   A.pg = p.packed;
@@ -1127,7 +1560,7 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
                                 void *args_buf) {
   search_args A{};
   A.hscr = static_cast<double *>(args_buf);
-  A.scr_warps = num_sms * 16;
+  A.scr_warps = num_sms * kMaxWarpsSM;
   A.b = b;
   A.p = p;
   A.pg = p.packed;

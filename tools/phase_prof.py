@@ -28,7 +28,7 @@ def main():
     lib = native.lib()
     fn = lib.vs_debug_phase_read
     fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-    buf = (C.c_ulonglong * 16)()
+    buf = (C.c_ulonglong * 24)()
     api.dock_and_score_batch(pocket, ligs, cfg, ctx)  # warm-up
     fn(buf, 1)
     r = api.dock_and_score_batch(pocket, ligs, cfg, ctx)
@@ -40,6 +40,9 @@ def main():
     print(f"per rebuild (max over lanes): sincos {buf[12] / nb:.0f}  chain {buf[13] / nb:.0f}  "
           f"rigid transforms {buf[14] / nb:.0f} cycles; whole rebuild phase {buf[9] / nb:.0f}; "
           f"of the chain: matrix setups {buf[15] / nb:.0f}")
+    if buf[17]:
+        print(f"screen: rows screened {buf[17]}, exact evaluations {buf[16]} ({buf[16] / max(buf[11], 1):.2f} per "
+              f"iteration, rigid {buf[18]})")
     for i, name in enumerate(NAMES):
         print(f"{name:32s} {100.0 * buf[i] / tot:6.2f} %   {buf[i] / 1e9:10.3f} Gcycles")
 
