@@ -329,3 +329,28 @@ class Oracle:
         self._build(el.size, abi.ptr(el, C.c_uint8), abi.ptr(xyz, C.c_double), abi.ptr(c, C.c_double),
                     radius, spacing, abi.ptr(dims, C.c_int32), abi.ptr(org, C.c_double), abi.ptr(vals, C.c_double))
         return Pocket(org, spacing, tuple(dims), vals, el, xyz, id="built")
+
+    # ------------------------------------------------------------ pipeline
+    def run_rank(self, data: bytes, pocket: Pocket, cfg: abi.ScoringConfig, slab=None, workers: int = 1,
+                 chunk_bytes: int = 1 << 20):
+        """The reference's own run_rank (pipeline.cpp:297-389; kind "ref"
+        only) over an in-memory .xslb image: (output text, counters dict)."""
+        assert self.kind == "ref"
+        f = self.lib.vsref_run_rank
+        f.restype = C.c_int
+        f.argtypes = [C.POINTER(C.c_uint8), C.c_int64, C.c_uint64, C.c_uint64, _PD, _CF, C.c_int, C.c_int64,
+                      C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        self.lib.vsref_free.argtypes = [C.c_void_p]
+        buf = np.frombuffer(data, dtype=np.uint8)
+        start, stop = slab if slab is not None else (0, len(data))
+        out = C.c_void_p()
+        n = C.c_int64()
+        cnt = (C.c_uint64 * 4)()
+        rc = f(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(data), start, stop, C.byref(pocket.desc()), C.byref(cfg),
+               workers, chunk_bytes, C.byref(out), C.byref(n), cnt)
+        if rc != abi.VS_OK:
+            raise ValueError(self._err().decode())
+        text = C.string_at(out, n.value).decode()
+        self.lib.vsref_free(out)
+        return text, dict(zip(("ligands_docked", "records_skipped", "dock_errors", "rows_written"), list(cnt)))
+

@@ -26,6 +26,7 @@
 #include "vscreen/geometry/transform.hpp"
 #include "vscreen/molmodel/binary_codec.hpp"
 #include "vscreen/molmodel/smiles.hpp"
+#include "vscreen/pipeline/pipeline.hpp"
 
 using namespace vscreen;
 
@@ -445,5 +446,42 @@ int vsref_build_pocket(int32_t n, const uint8_t *elem, const double *xyz, const 
     return VS_ERR_INVALID_ARGUMENT;
   }
 }
+
+// run_rank (pipeline.cpp:297-398) over an in-memory .xslb image: the
+// reference's reader / splitter / `workers` docker threads / writer.  The
+// rank's output text goes to *out (malloc'ed, caller frees with
+// vsref_free); counters: ligands_docked, records_skipped, dock_errors,
+// rows_written.  Returns VS_OK or VS_ERR_INVALID_ARGUMENT (message in
+// vsref_last_error).
+int vsref_run_rank(const uint8_t *bytes, int64_t size, uint64_t slab_start, uint64_t slab_stop,
+                   const vs_pocket_desc *pd, const vs_scoring_config *cfg, int workers, int64_t chunk_bytes,
+                   char **out, int64_t *out_len, uint64_t counters[4]) {
+  try {
+    const Pocket pocket = pocket_from_desc(pd);
+    PipelineConfig pc;
+    pc.scoring = to_cfg(cfg);
+    pc.workers = {WorkerClass{WorkerKind::Fast, workers, 1.0}};
+    pc.chunk_bytes = static_cast<std::size_t>(chunk_bytes);
+    MemorySource src(std::vector<std::uint8_t>(bytes, bytes + size));
+    StringSink sink;
+    RankPlan plan;
+    plan.slab_start = slab_start;
+    plan.slab_stop = slab_stop;
+    const RankStats st = run_rank(plan, src, sink, pocket, pc);
+    *out_len = static_cast<int64_t>(sink.data().size());
+    *out = static_cast<char *>(std::malloc(sink.data().size() + 1));
+    std::memcpy(*out, sink.data().data(), sink.data().size());
+    counters[0] = st.ligands_docked;
+    counters[1] = st.records_skipped;
+    counters[2] = st.dock_errors;
+    counters[3] = st.rows_written;
+    return VS_OK;
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return VS_ERR_INVALID_ARGUMENT;
+  }
+}
+
+void vsref_free(void *p) { std::free(p); }
 
 }  // extern "C"

@@ -159,6 +159,29 @@ POSE_DTYPE = np.dtype(
 assert POSE_DTYPE.itemsize == C.sizeof(PoseDesc)
 
 
+class RankConfig(C.Structure):
+    """vs_rank_config (include/vs_rank.h)."""
+    _fields_ = [("n_devices", C.c_int32), ("devices", C.POINTER(C.c_int32)), ("workers_per_device", C.c_int32),
+                ("batch_records", C.c_int32), ("chunk_bytes", C.c_int64), ("writer_buffer_bytes", C.c_int64)]
+
+
+class RankStats(C.Structure):
+    """vs_rank_stats = RankStats (pipeline.hpp:96-115) + GPU batch counters."""
+    _fields_ = [(f, C.c_uint64) for f in ("ligands_docked", "records_skipped", "dock_errors", "rows_written",
+                                          "chunks_read", "bytes_read", "write_calls", "bytes_written")] + \
+               [("workers", C.c_int32)] + \
+               [(f, C.c_double) for f in ("wall_seconds", "reader_busy_seconds", "splitter_busy_seconds",
+                                          "docker_busy_seconds", "writer_busy_seconds")] + \
+               [("batches", C.c_uint64), ("resyncs", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+READ_FN = C.CFUNCTYPE(C.c_int64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint8), C.c_int64)
+WRITE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_char), C.c_int64)
+
+
 def ptr(a: np.ndarray | None, ctype):
     """Pointer to a contiguous numpy array (None -> NULL)."""
     if a is None:

@@ -525,3 +525,54 @@ def dock_and_score(pocket, ligand: Ligand, config: ScoringConfig | None = None,
     if st not in (abi.VS_LIG_OK, abi.VS_LIG_NONFINITE):
         raise ValueError(abi.LIGAND_STATUS_NAMES.get(st, f"ligand status {st}"))
     return br.result(0)
+
+
+# ---------------------------------------------------------------- pipeline rank
+XSLB_HEADER = bytes([0x58, 0x53, 0x4C, 0x42, 1, 0, 0, 0])  # xslb_header(): magic "XSLB", version 1
+
+
+def plan_slabs(file_size: int, n_ranks: int) -> list[tuple[int, int]]:
+    """plan_slabs (pipeline.cpp:32-45): rank i owns record starts in
+    [size * i / n, size * (i + 1) / n)."""
+    if n_ranks < 1:
+        raise ValueError("rank count must be at least 1")
+    return [(file_size * i // n_ranks, file_size * (i + 1) // n_ranks) for i in range(n_ranks)]
+
+
+def run_rank(data: bytes, pocket, config: ScoringConfig | None = None, slab: tuple[int, int] | None = None,
+             devices=None, workers_per_device: int = 2, batch_records: int = 32768, chunk_bytes: int = 1 << 20,
+             writer_buffer_bytes: int = 4 << 20):
+    """run_rank (pipeline.cpp:297-389) of one slab of an in-memory .xslb image
+    on the B200 CUDA workers (vs_run_rank): returns (output text, RankStats
+    dict).  `pocket` is a host Pocket (model.Pocket); rows are format_row
+    lines in record order."""
+    buf = np.frombuffer(data, dtype=np.uint8)
+    start, stop = slab if slab is not None else (0, len(data))
+    parts = []
+
+    def _read(_u, off, out, n):
+        n = max(0, min(n, len(data) - off))
+        C.memmove(out, buf.ctypes.data + off, n)
+        return n
+
+    def _write(_u, p, n):
+        parts.append(C.string_at(p, n))
+        return 0
+
+    rf, wf = abi.READ_FN(_read), abi.WRITE_FN(_write)
+    rc = abi.RankConfig()
+    native.lib().vs_rank_config_default(C.byref(rc))
+    dev_arr = None
+    if devices is not None:
+        dev_arr = (C.c_int32 * len(devices))(*devices)
+        rc.n_devices = len(devices)
+        rc.devices = C.cast(dev_arr, C.POINTER(C.c_int32))
+    rc.workers_per_device = workers_per_device
+    rc.batch_records = batch_records
+    rc.chunk_bytes = chunk_bytes
+    rc.writer_buffer_bytes = writer_buffer_bytes
+    st = abi.RankStats()
+    cfg = config or ScoringConfig()
+    native.check(native.lib().vs_run_rank(len(data), rf, None, start, stop, C.byref(pocket.desc()), C.byref(cfg),
+                                          C.byref(rc), wf, None, C.byref(st)), "vs_run_rank")
+    return b"".join(parts).decode(), st.as_dict()

@@ -15,7 +15,9 @@
 // reference treats Pocket as immutable and shared).
 #include <algorithm>
 #include <cmath>
+#include <charconv>
 #include <cstring>
+#include <fstream>
 #include <limits>
 #include <map>
 #include <mutex>
@@ -27,10 +29,12 @@
 
 #include "vs_dock.h"
 #include "vs_prep.h"
+#include "vs_rank.h"
 #include "vscreen/dockengine/chem.hpp"
 #include "vscreen/dockengine/grid.hpp"
 #include "vscreen/dockengine/search.hpp"
 #include "vscreen/error.hpp"
+#include "vscreen/pipeline/pipeline.hpp"
 
 namespace vscreen {
 namespace {
@@ -663,6 +667,189 @@ Pose exhaustive_dock(const Pocket &pocket, const Ligand &ligand) {
   pose.conformation = apply_rigid(base, pose.transform);
   pose.geo_score = geo_score(pocket, ligand, pose.conformation);
   return pose;
+}
+
+}  // namespace vscreen
+
+// ------------------------------------------------------------ pipeline
+namespace vscreen {
+
+// io.hpp: sources and sinks
+std::size_t MemorySource::read_at(std::uint64_t offset, std::span<std::uint8_t> out) {
+  if (offset >= bytes_.size()) return 0;
+  const std::size_t n = std::min<std::size_t>(out.size(), bytes_.size() - static_cast<std::size_t>(offset));
+  std::memcpy(out.data(), bytes_.data() + offset, n);
+  return n;
+}
+
+FileSource::FileSource(const std::string &path) : in_(path, std::ios::binary), path_(path) {
+  if (!in_) throw IoError("cannot open input '" + path + "'");
+  in_.seekg(0, std::ios::end);
+  size_ = static_cast<std::uint64_t>(in_.tellg());
+}
+
+std::size_t FileSource::read_at(std::uint64_t offset, std::span<std::uint8_t> out) {
+  if (offset >= size_) return 0;
+  in_.clear();
+  in_.seekg(static_cast<std::streamoff>(offset));
+  in_.read(reinterpret_cast<char *>(out.data()), static_cast<std::streamsize>(out.size()));
+  if (in_.bad()) throw IoError("read failed on '" + path_ + "'");
+  return static_cast<std::size_t>(in_.gcount());
+}
+
+FileSink::FileSink(const std::string &path) : out_(path, std::ios::binary | std::ios::trunc), path_(path) {
+  if (!out_) throw IoError("cannot open output '" + path + "'");
+}
+
+void FileSink::write(std::string_view bytes) {
+  out_.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+  if (!out_) throw IoError("write failed on '" + path_ + "'");
+}
+
+void FileSink::finish() {
+  out_.flush();
+  if (!out_) throw IoError("cannot finish output '" + path_ + "'");
+}
+
+std::vector<RankPlan> plan_slabs(std::uint64_t file_size, int n_ranks) {
+  if (n_ranks < 1) throw InvalidArgument("rank count must be at least 1");
+  std::vector<RankPlan> plans(static_cast<std::size_t>(n_ranks));
+  for (int i = 0; i < n_ranks; ++i) {
+    RankPlan &p = plans[static_cast<std::size_t>(i)];
+    p.rank = i;
+    p.n_ranks = n_ranks;
+    p.slab_start = file_size * static_cast<std::uint64_t>(i) / static_cast<std::uint64_t>(n_ranks);
+    p.slab_stop = file_size * static_cast<std::uint64_t>(i + 1) / static_cast<std::uint64_t>(n_ranks);
+  }
+  return plans;
+}
+
+std::string format_row(const OutputRow &row) {
+  if (!std::isfinite(row.score)) throw InvalidArgument("output row score must be finite");
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof buf, row.score, std::chars_format::fixed, 4);
+  if (r.ec != std::errc()) throw InvalidArgument("output row score does not format");
+  std::string line = row.smiles;
+  line += '\t';
+  line.append(buf, r.ptr);
+  line += '\n';
+  return line;
+}
+
+namespace {
+struct RankIo {
+  ByteSource *src;
+  Sink *sink;
+  std::string error;
+};
+int64_t rank_read(void *u, uint64_t off, uint8_t *out, int64_t n) {
+  auto *io = static_cast<RankIo *>(u);
+  try {
+    return static_cast<int64_t>(io->src->read_at(off, std::span<std::uint8_t>(out, static_cast<std::size_t>(n))));
+  } catch (const std::exception &e) {
+    io->error = e.what();
+    return -1;
+  }
+}
+int32_t rank_write(void *u, const char *b, int64_t n) {
+  auto *io = static_cast<RankIo *>(u);
+  try {
+    io->sink->write(std::string_view(b, static_cast<std::size_t>(n)));
+    return 0;
+  } catch (const std::exception &e) {
+    io->error = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+RankStats run_rank(const RankPlan &plan, ByteSource &source, Sink &sink, const Pocket &pocket,
+                   const PipelineConfig &config) {
+  int total = 0;
+  for (const WorkerClass &wc : config.workers) {
+    if (wc.count < 0) throw InvalidArgument("worker count must not be negative");
+    if (wc.synthetic_slowdown < 1.0) throw InvalidArgument("synthetic slowdown must be at least 1");
+    total += wc.count;
+  }
+  if (total < 1) throw InvalidArgument("need at least one worker");
+  if (config.chunk_bytes == 0) throw InvalidArgument("chunk size must be positive");
+  if (plan.slab_start > plan.slab_stop) throw InvalidArgument("slab start past slab stop");
+  if (plan.slab_stop > source.size()) throw InvalidArgument("slab exceeds the input size");
+  std::vector<uint8_t> el;
+  std::vector<double> xyz;
+  for (const ProteinAtom &a : pocket.protein_atoms) {
+    el.push_back(static_cast<uint8_t>(a.element));
+    xyz.insert(xyz.end(), {a.position.x(), a.position.y(), a.position.z()});
+  }
+  vs_pocket_desc d{};
+  for (int a = 0; a < 3; ++a) {
+    d.origin[a] = pocket.origin[a];
+    d.dims[a] = pocket.dims[a];
+  }
+  d.spacing = pocket.spacing;
+  d.values = pocket.values.data();
+  d.n_protein = static_cast<int32_t>(el.size());
+  d.protein_element = el.empty() ? nullptr : el.data();
+  d.protein_xyz = xyz.empty() ? nullptr : xyz.data();
+  vs_rank_config rc;
+  vs_rank_config_default(&rc);
+  int32_t dev = 0;
+  if (tl_device >= 0) {  // the calling thread pinned a GPU (b200::use_device)
+    dev = tl_device;
+    rc.n_devices = 1;
+    rc.devices = &dev;
+  }
+  rc.workers_per_device = total;
+  rc.chunk_bytes = static_cast<int64_t>(config.chunk_bytes);
+  rc.writer_buffer_bytes = static_cast<int64_t>(std::max<std::size_t>(config.writer_buffer_bytes, 1));
+  const vs_scoring_config cfg = to_c(config.scoring);
+  RankIo io{&source, &sink, {}};
+  vs_rank_stats st{};
+  const vs_status rs = vs_run_rank(source.size(), rank_read, &io, plan.slab_start, plan.slab_stop, &d, &cfg, &rc,
+                                   rank_write, &io, &st);
+  if (!io.error.empty()) throw IoError(io.error);
+  if (rs == VS_ERR_INVALID_ARGUMENT) {
+    const std::string msg = last_error();
+    if (msg.rfind("corrupt record stream", 0) == 0) throw CodecError(msg);
+    throw InvalidArgument(msg);
+  }
+  check(rs, "run_rank");
+  sink.finish();
+  RankStats out;
+  out.ligands_docked = st.ligands_docked;
+  out.records_skipped = st.records_skipped;
+  out.dock_errors = st.dock_errors;
+  out.rows_written = st.rows_written;
+  out.chunks_read = st.chunks_read;
+  out.bytes_read = st.bytes_read;
+  out.write_calls = st.write_calls;
+  out.bytes_written = st.bytes_written;
+  out.workers = st.workers;
+  out.wall_seconds = st.wall_seconds;
+  out.reader_busy_seconds = st.reader_busy_seconds;
+  out.splitter_busy_seconds = st.splitter_busy_seconds;
+  out.docker_busy_seconds = st.docker_busy_seconds;
+  out.writer_busy_seconds = st.writer_busy_seconds;
+  return out;
+}
+
+RankStats run_rank(const RankPlan &plan, const Pocket &pocket, const PipelineConfig &config) {
+  FileSource source(plan.input_path);
+  FileSink sink(plan.output_path);
+  return run_rank(plan, source, sink, pocket, config);
+}
+
+void merge_outputs(const std::vector<std::string> &paths, const std::string &merged_path) {
+  std::ofstream out(merged_path, std::ios::binary | std::ios::trunc);
+  if (!out) throw IoError("cannot open merged output '" + merged_path + "'");
+  for (const std::string &path : paths) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("missing rank output '" + path + "'");
+    out << in.rdbuf();
+    if (in.bad() || !out) throw IoError("merge failed while copying '" + path + "'");
+  }
+  out.flush();
+  if (!out) throw IoError("cannot finish merged output '" + merged_path + "'");
 }
 
 }  // namespace vscreen

@@ -21,6 +21,7 @@
 #include "../../../include/vs_crtrig.h"
 #include "../../../include/vs_codec.h"
 #include "../../../include/vs_dock.h"
+#include "../../../include/vs_rank.h"
 #include "../host/ligand_set.hpp"
 #include "kernels.cuh"
 
@@ -696,6 +697,21 @@ int vs_device_count(void) {
 }
 
 const char *vs_last_error_message(void) { return g_err.c_str(); }
+
+// Host-side components of the library (host/rank.cpp) report errors through
+// the same thread-local message.
+vs_status vs_internal_fail(vs_status s, const char *msg) { return fail(s, msg ? msg : ""); }
+
+vs_status vs_host_alloc(size_t bytes, void **out) {
+  if (!out) return fail(VS_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  CUDA_TRY(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+  return VS_OK;
+}
+
+void vs_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+}
 
 void vs_scoring_config_default(vs_scoring_config *c) {
   c->restarts = 256;

@@ -24,8 +24,8 @@ _DR = C.POINTER(abi.DockResult)
 _PO = C.POINTER(abi.PoseDesc)
 _vp = C.c_void_p
 
-# (name, restype, argtypes) for every entry point of include/vs_dock.h and
-# include/vs_prep.h.
+# (name, restype, argtypes) for every entry point of include/vs_dock.h,
+# vs_prep.h, vs_codec.h and vs_rank.h.
 SIGNATURES = {
     "vs_abi_version": (C.c_int, []),
     "vs_device_count": (C.c_int, []),
@@ -68,6 +68,12 @@ SIGNATURES = {
     "vs_dock_records": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, C.POINTER(C.c_uint8), C.c_int64,
                                   C.POINTER(C.c_int64), C.c_int32, _CF, _DR, C.POINTER(C.c_int32)]),
     "vs_ligand_set_free": (None, [_vp]),
+    # vs_rank.h
+    "vs_rank_config_default": (None, [C.POINTER(abi.RankConfig)]),
+    "vs_run_rank": (C.c_int, [C.c_uint64, abi.READ_FN, _vp, C.c_uint64, C.c_uint64, _PD, _CF,
+                              C.POINTER(abi.RankConfig), abi.WRITE_FN, _vp, C.POINTER(abi.RankStats)]),
+    "vs_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "vs_host_free": (None, [_vp]),
     "vs_detect_torsions": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint8)]),
     "vs_bridge_bonds": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint8)]),
     "vs_synth_smiles": (C.c_int64, [C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

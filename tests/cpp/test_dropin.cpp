@@ -2,6 +2,7 @@
 // (proj/include/vscreen) runs unchanged on the B200 build (libvscreen_b200).
 // Mirrors checks of test_dockengine.cpp / test_ligand_graph.cpp.
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -11,10 +12,46 @@
 #include "vscreen/dockengine/grid.hpp"
 #include "vscreen/dockengine/search.hpp"
 #include "vscreen/error.hpp"
+#include "vscreen/pipeline/pipeline.hpp"
 
 using namespace vscreen;
 
 static int failures = 0;
+
+// encode_record (binary_codec.cpp:129-163), for building an .xslb image
+static void put16(std::vector<std::uint8_t> &o, unsigned v) {
+  o.push_back(v & 255);
+  o.push_back((v >> 8) & 255);
+}
+static void encode(std::vector<std::uint8_t> &o, const vscreen::Ligand &l) {
+  std::vector<std::uint8_t> p;
+  put16(p, static_cast<unsigned>(l.name.size()));
+  p.insert(p.end(), l.name.begin(), l.name.end());
+  put16(p, static_cast<unsigned>(l.atoms.size()));
+  put16(p, static_cast<unsigned>(l.bonds.size()));
+  put16(p, static_cast<unsigned>(l.torsions.size()));
+  for (const auto &a : l.atoms) {
+    for (int k = 0; k < 3; ++k) {
+      const float f = static_cast<float>(a.position[k]);
+      std::uint8_t b[4];
+      std::memcpy(b, &f, 4);
+      p.insert(p.end(), b, b + 4);
+    }
+    p.push_back(static_cast<std::uint8_t>(a.element));
+    p.push_back(a.is_heavy ? 1 : 0);
+  }
+  for (const auto &b : l.bonds) {
+    put16(p, b.a);
+    put16(p, b.b);
+    p.push_back(static_cast<std::uint8_t>(b.order));
+  }
+  for (const auto &t : l.torsions) put16(p, t.bond_index);
+  o.push_back(0xD0);
+  o.push_back(0xC5);
+  const std::uint32_t n = static_cast<std::uint32_t>(p.size());
+  for (int k = 0; k < 4; ++k) o.push_back((n >> (8 * k)) & 255);
+  o.insert(o.end(), p.begin(), p.end());
+}
 #define CHECK(x)                                                     \
   do {                                                               \
     if (!(x)) {                                                      \
@@ -141,6 +178,31 @@ int main() {
     CHECK(pocket_field_value(pm, mid.col(0)) == 0.0);
     pm.values[pm.value_index(1, 1, 1)] = 5.0;  // mutated in place: same buffer, same sizes
     CHECK(pocket_field_value(pm, mid.col(0)) == 5.0);
+  }
+
+  // run_rank on the CUDA workers (pipeline.cpp:297-389): rows equal
+  // format_row of dock_and_score per record, in record order
+  {
+    std::vector<std::uint8_t> img = {'X', 'S', 'L', 'B', 1, 0, 0, 0};
+    std::vector<Ligand> lib = b200::prepare_ligands({"CCOC(=O)c1ccccc1N", "CCCCCCO", "c1ccccc1-c1ccccc1"});
+    const char *names[] = {"CCOC(=O)c1ccccc1N", "CCCCCCO", "c1ccccc1-c1ccccc1"};
+    for (std::size_t i = 0; i < lib.size(); ++i) {
+      lib[i].name = names[i];
+      encode(img, lib[i]);
+    }
+    std::string want;
+    for (const Ligand &l : lib) want += format_row(OutputRow{l.name, dock_and_score(twin, l, cfg).best_score});
+    MemorySource src(img);
+    StringSink sink;
+    RankPlan plan;
+    plan.slab_stop = src.size();
+    PipelineConfig pc;
+    pc.scoring = cfg;
+    pc.workers = {WorkerClass{WorkerKind::Fast, 2, 1.0}};
+    const RankStats rs = run_rank(plan, src, sink, twin, pc);
+    CHECK(sink.data() == want);
+    CHECK(rs.rows_written == 3 && rs.ligands_docked == 3 && rs.records_skipped == 0 && rs.dock_errors == 0);
+    CHECK(plan_slabs(10, 3)[1].slab_start == 3 && plan_slabs(10, 3)[2].slab_stop == 10);
   }
 
   // per-thread device selection

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     syms = set()
-    for h in ("vs_dock.h", "vs_prep.h", "vs_codec.h"):
+    for h in ("vs_dock.h", "vs_prep.h", "vs_codec.h", "vs_rank.h"):
         text = open(os.path.join(ROOT, "include", h)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         syms |= set(re.findall(r"\b(vs_[a-z0-9_]+)\s*\(", text))
