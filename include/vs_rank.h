@@ -76,6 +76,14 @@ vs_status vs_run_rank(uint64_t source_size, vs_read_fn read, void *read_user, ui
                       uint64_t slab_stop, const vs_pocket_desc *pocket, const vs_scoring_config *cfg,
                       const vs_rank_config *rc, vs_write_fn write, void *write_user, vs_rank_stats *stats);
 
+/* The campaign ranking (cmd_merge, merge.cpp:81-147): every row of the
+ * n_files score texts (rank order) stable-sorted by (printed score desc,
+ * SMILES asc) and written as the original row text, one per line; only the
+ * first top_k rows when top_k >= 0.  Parallel run sorts on `threads` host
+ * threads (0 = all) + a stable k-way merge.  *rows_out = rows written. */
+vs_status vs_merge_rankings(const char *const *texts, const int64_t *lens, int32_t n_files, int64_t top_k,
+                            int32_t threads, vs_write_fn write, void *user, uint64_t *rows_out);
+
 /* Pinned (page-locked) host memory for callers that stage their own batches. */
 vs_status vs_host_alloc(size_t bytes, void **out);
 void vs_host_free(void *p);

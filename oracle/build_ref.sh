@@ -15,7 +15,7 @@ fi
 mkdir -p "$HERE/_ref/obj"
 SRCS="dockengine/chem dockengine/grid dockengine/search dockengine/pocket_io
       geometry/transform geometry/embed geometry/hydrogens
-      molmodel/ligand molmodel/binary_codec molmodel/smiles pipeline/pipeline pipeline/io"
+      molmodel/ligand molmodel/binary_codec molmodel/smiles pipeline/pipeline pipeline/io workflow/merge"
 FLAGS=(-std=c++20 -O3 -fPIC -w -I"$HERE/../third_party/eigen_subset" -I"$REF/include" -I"$HERE/../include")
 pids=()
 for s in $SRCS; do

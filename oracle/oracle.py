@@ -354,3 +354,24 @@ class Oracle:
         self.lib.vsref_free(out)
         return text, dict(zip(("ligands_docked", "records_skipped", "dock_errors", "rows_written"), list(cnt)))
 
+    def cmd_merge(self, out_dir: str) -> int:
+        """The reference's cmd_merge (merge.cpp:81-147): writes
+        <out_dir>/ranking.tsv from job.txt + rank<i>.scores/.stats."""
+        assert self.kind == "ref"
+        f = self.lib.vsref_cmd_merge
+        f.restype = C.c_int64
+        f.argtypes = [C.c_char_p]
+        n = f(out_dir.encode())
+        if n < 0:
+            raise ValueError(self._err().decode())
+        return int(n)
+
+    def format_rank_stats(self, counters) -> str:
+        f = self.lib.vsref_format_rank_stats
+        f.restype = C.c_int64
+        f.argtypes = [C.POINTER(C.c_uint64), C.c_char_p, C.c_int64]
+        cnt = (C.c_uint64 * 4)(*counters)
+        buf = C.create_string_buffer(4096)
+        n = f(cnt, buf, 4096)
+        return buf.raw[:n].decode()
+

@@ -27,6 +27,7 @@
 #include "vscreen/molmodel/binary_codec.hpp"
 #include "vscreen/molmodel/smiles.hpp"
 #include "vscreen/pipeline/pipeline.hpp"
+#include "vscreen/workflow/workflow.hpp"
 
 using namespace vscreen;
 
@@ -480,6 +481,31 @@ int vsref_run_rank(const uint8_t *bytes, int64_t size, uint64_t slab_start, uint
     g_err = e.what();
     return VS_ERR_INVALID_ARGUMENT;
   }
+}
+
+// cmd_merge (merge.cpp:81-147) of a campaign directory: writes
+// <out_dir>/ranking.tsv; returns the row count, or -1 (message in
+// vsref_last_error).
+int64_t vsref_cmd_merge(const char *out_dir) {
+  try {
+    return static_cast<int64_t>(cmd_merge(out_dir).rows);
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// format_rank_stats (pipeline.cpp:430) of a RankStats with the four counters.
+int64_t vsref_format_rank_stats(const uint64_t counters[4], char *out, int64_t cap) {
+  RankStats st;
+  st.ligands_docked = counters[0];
+  st.records_skipped = counters[1];
+  st.dock_errors = counters[2];
+  st.rows_written = counters[3];
+  const std::string t = format_rank_stats(st);
+  if (static_cast<int64_t>(t.size()) > cap) return -static_cast<int64_t>(t.size());
+  std::memcpy(out, t.data(), t.size());
+  return static_cast<int64_t>(t.size());
 }
 
 void vsref_free(void *p) { std::free(p); }

@@ -576,3 +576,22 @@ def run_rank(data: bytes, pocket, config: ScoringConfig | None = None, slab: tup
     native.check(native.lib().vs_run_rank(len(data), rf, None, start, stop, C.byref(pocket.desc()), C.byref(cfg),
                                           C.byref(rc), wf, None, C.byref(st)), "vs_run_rank")
     return b"".join(parts).decode(), st.as_dict()
+
+
+def merge_rankings(texts, top_k: int = -1, threads: int = 0) -> tuple[str, int]:
+    """cmd_merge's ranking (merge.cpp:81-147) of rank score texts in rank
+    order, natively (vs_merge_rankings): (ranking text, rows)."""
+    bs = [t.encode() if isinstance(t, str) else bytes(t) for t in texts]
+    arr = (C.c_char_p * max(len(bs), 1))(*bs)
+    lens = (C.c_int64 * max(len(bs), 1))(*[len(b) for b in bs])
+    parts = []
+
+    def _write(_u, p, n):
+        parts.append(C.string_at(p, n))
+        return 0
+
+    wf = abi.WRITE_FN(_write)
+    rows = C.c_uint64()
+    native.check(native.lib().vs_merge_rankings(arr, lens, len(bs), top_k, threads, wf, None, C.byref(rows)),
+                 "vs_merge_rankings")
+    return b"".join(parts).decode(), int(rows.value)

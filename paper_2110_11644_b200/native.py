@@ -72,6 +72,8 @@ SIGNATURES = {
     "vs_rank_config_default": (None, [C.POINTER(abi.RankConfig)]),
     "vs_run_rank": (C.c_int, [C.c_uint64, abi.READ_FN, _vp, C.c_uint64, C.c_uint64, _PD, _CF,
                               C.POINTER(abi.RankConfig), abi.WRITE_FN, _vp, C.POINTER(abi.RankStats)]),
+    "vs_merge_rankings": (C.c_int, [C.POINTER(C.c_char_p), C.POINTER(C.c_int64), C.c_int32, C.c_int64, C.c_int32,
+                                    abi.WRITE_FN, _vp, C.POINTER(C.c_uint64)]),
     "vs_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "vs_host_free": (None, [_vp]),
     "vs_detect_torsions": (C.c_int32, [_LB, C.c_int32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint8)]),

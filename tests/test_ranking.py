@@ -1,0 +1,66 @@
+"""Campaign ranking: the native merge
+(vs_merge_rankings) produces exactly the reference's cmd_merge ranking
+(merge.cpp:81-147, compiled from its sources into oracle/_ref) and the
+Python ranking module's order, with exact score ties across rank files."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import Oracle, available
+from paper_2110_11644_b200 import api, ranking
+
+
+def rank_texts(n_files: int, rows: int, seed: int):
+    rng = np.random.default_rng(seed)
+    texts, allrows = [], []
+    for _ in range(n_files):
+        sc = np.round(rng.normal(20, 5, rows), 2)  # 2 decimals: many exact ties
+        smi = [f"C{'C' * int(k % 7)}O{int(k)}" for k in rng.integers(0, 20000, rows)]  # duplicate SMILES too
+        texts.append("".join(ranking.format_row(s, float(x)) for s, x in zip(smi, sc)))
+        allrows += list(zip(smi, sc.tolist()))
+    return texts, allrows
+
+
+def python_ranking(allrows):
+    keys = [ranking.row_key(x, s) for s, x in allrows]
+    order = sorted(range(len(keys)), key=lambda i: (-keys[i][0], keys[i][1].encode()))  # stable
+    return "".join(ranking.format_row(allrows[i][0], allrows[i][1]) for i in order)
+
+
+def test_native_merge_equals_python_ranking():
+    texts, allrows = rank_texts(5, 40_000, 3)
+    got, n = api.merge_rankings(texts, threads=4)
+    assert n == 200_000
+    assert got == python_ranking(allrows)
+    top, k = api.merge_rankings(texts, top_k=1000)
+    assert k == 1000 and top == "".join(got.splitlines(keepends=True)[:1000])
+
+
+def test_native_merge_rejects_bad_rows():
+    with pytest.raises(ValueError, match="tab"):
+        api.merge_rankings(["CCO 1.0\n"])
+    with pytest.raises(ValueError, match="bad score"):
+        api.merge_rankings(["CCO\t1.0x\n"])
+    assert api.merge_rankings([]) == ("", 0)
+
+
+@pytest.mark.skipif(not available("ref"), reason="oracle/_ref not built")
+def test_native_merge_equals_reference_cmd_merge(tmp_path):
+    ref = Oracle("ref")
+    texts, _ = rank_texts(3, 20_000, 7)
+    d = str(tmp_path)
+    with open(os.path.join(d, "job.txt"), "w") as f:
+        f.write(f"ranks={len(texts)}\n")
+    for r, t in enumerate(texts):
+        with open(os.path.join(d, f"rank{r}.scores"), "w") as f:
+            f.write(t)
+        with open(os.path.join(d, f"rank{r}.stats"), "w") as f:
+            n = t.count("\n")
+            f.write(ref.format_rank_stats([n, 0, 0, n]))
+    assert ref.cmd_merge(d) == 60_000
+    want = open(os.path.join(d, "ranking.tsv")).read()
+    got, n = api.merge_rankings(texts)
+    assert n == 60_000 and got == want
