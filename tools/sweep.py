@@ -57,7 +57,7 @@ def main():
             ligs = api.prepare_ligand(smi, quantize=True, ctx=ctx, nthreads=threads)
             prep_s = time.perf_counter() - t0
             batch = LigandBatch(ligs)
-            api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False)  # warm-up
+            api.dock_and_score_batch(pocket, LigandBatch(ligs[:2048]), cfg, ctx, want_conformation=False)  # warm-up
             r = api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False)
             line = {**cell, "ligands": len(ligs), "gpu_ligands_per_s": len(ligs) / (r.kernel_ms / 1e3),
                     "stage_ms": {k: round(v, 2) for k, v in r.stage_ms.items()},
