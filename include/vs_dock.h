@@ -240,6 +240,9 @@ vs_status vs_dock_batch_multi(vs_context *ctx, const vs_pocket *const *pockets, 
 /* Measured FP64 DADD ops/s, FP64 DFMA flop/s and FP32 FFMA flop/s of the
  * device (the roofline denominators of this CUDA-core path). */
 int vs_measure_peaks(int device, double out[3]);
+/* Random-gather rate (loads/s) of elem_bytes-byte loads (2, 4, 16, 32) over a
+ * ws_bytes L1/L2-resident working set: the sampler's gather roofline. */
+int vs_measure_gather(int device, int64_t ws_bytes, int32_t elem_bytes, double *loads_per_s);
 
 /* Device self-test of the branch-free square root used by the kernels
  * (dmath.cuh dsqrt) against the IEEE sqrt: n inputs drawn from seed (random

@@ -56,6 +56,37 @@ __global__ void k_ffma(float *out, int iters, float a, float c) {
   if (s == 1234.5f) out[0] = s;
 }
 
+// Random gathers over an L1/L2-resident working set (the
+// sampler's cell-word and corner loads): every thread runs 8 independent
+// LCG address streams; E = 2, 4, 16 or 32 bytes per load (32 = two
+// adjacent 16-byte loads, one 32-byte sector).
+template <int E>
+__global__ void k_gather(const uint4 *buf, uint32_t mask, int iters, uint32_t *out) {
+  uint32_t st[kChains], acc = 0;
+#pragma unroll
+  for (int j = 0; j < kChains; ++j) st[j] = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + j * 40503u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < kChains; ++j) {
+      st[j] = st[j] * 1664525u + 1013904223u;
+      const uint32_t idx = (st[j] >> 4) & mask;
+      if (E == 2) {
+        acc += __ldg(reinterpret_cast<const uint16_t *>(buf) + idx);
+      } else if (E == 4) {
+        acc += __ldg(reinterpret_cast<const uint32_t *>(buf) + idx);
+      } else if (E == 16) {
+        const uint4 v = __ldg(buf + idx);
+        acc += v.x ^ v.w;
+      } else {
+        const uint4 v = __ldg(buf + 2 * idx), w = __ldg(buf + 2 * idx + 1);
+        acc += v.x ^ w.w;
+      }
+      st[j] ^= acc & 1u;  // keep the loads live without serialising the chains
+    }
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
 template <typename F>
 double rate(F launch, double ops) {
   cudaEvent_t a, b;
@@ -199,3 +230,34 @@ extern "C" int vs_measure_peaks(int device, double out[3]) {
   cudaFree(dbuf);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
+
+// Random-gather rate (loads per second) of E-byte loads over a ws_bytes
+// working set (rounded down to a power of two elements).
+extern "C" int vs_measure_gather(int device, int64_t ws_bytes, int32_t elem_bytes, double *loads_per_s) {
+  if (cudaSetDevice(device) != cudaSuccess) return 2;
+  if (!loads_per_s || (elem_bytes != 2 && elem_bytes != 4 && elem_bytes != 16 && elem_bytes != 32)) return 1;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  uint64_t elems = 1;
+  while (elems * 2 * elem_bytes <= (uint64_t)ws_bytes) elems *= 2;
+  uint4 *buf = nullptr;
+  if (cudaMalloc(&buf, elems * elem_bytes + 64) != cudaSuccess) return 3;
+  cudaMemset(buf, 1, elems * elem_bytes + 64);
+  uint32_t *out = nullptr;
+  cudaMalloc(&out, 64);
+  const int blocks = sms * 8, threads = 256, iters = 256;
+  const uint32_t mask = (uint32_t)(elems - 1);
+  const double loads = (double)blocks * threads * iters * kChains;
+  double r = 0.0;
+  switch (elem_bytes) {
+    case 2: r = rate([&] { k_gather<2><<<blocks, threads>>>(buf, mask, iters, out); }, loads); break;
+    case 4: r = rate([&] { k_gather<4><<<blocks, threads>>>(buf, mask, iters, out); }, loads); break;
+    case 16: r = rate([&] { k_gather<16><<<blocks, threads>>>(buf, mask, iters, out); }, loads); break;
+    default: r = rate([&] { k_gather<32><<<blocks, threads>>>(buf, mask, iters, out); }, loads); break;
+  }
+  *loads_per_s = r;
+  cudaFree(buf);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+

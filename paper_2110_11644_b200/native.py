@@ -52,6 +52,7 @@ SIGNATURES = {
     "vs_cluster_select": (C.c_int, [_vp, _LB, C.c_int32, _d, _d, C.c_double, C.c_int32, _i32, _i32]),
     "vs_local_search_batch": (C.c_int, [_vp, _vp, _LB, _CF, _PO, _d, _d, _u64, _i32]),
     "vs_measure_peaks": (C.c_int, [C.c_int, _d]),
+    "vs_measure_gather": (C.c_int, [C.c_int, C.c_int64, C.c_int32, _d]),
     "vs_selftest_sqrt": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), _d]),
     "vs_selftest_div": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), _d]),
     # vs_prep.h
