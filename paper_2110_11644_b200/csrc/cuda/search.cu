@@ -191,7 +191,7 @@ struct search_args {
   // FP32 screen (SCR): heavy frame, torsion-neighbour matrices + their error
   // constants, the 13 rigid maps (12 neighbours + current pose), the exact
   // candidate row, FP32 current samples, FP32 stage-t prefixes
-  int o_t32, o_M32, o_kap, o_A32, o_vex, o_vc32, o_pc32;
+  int o_t32, o_A32, o_vc32, o_crow;
   size_t scr_stride;     // doubles of global scratch per warp
 };
 
@@ -305,7 +305,7 @@ __device__ __noinline__ void hydrogen_frame(double *hx, int N, const double *bas
 // is the same for (t,+) and (t,-) and for every step level), pairs from
 // `pfrom` on.  Recomputed only when a torsion move changes Mcur.
 __device__ __noinline__ void prefix_frame(double *pc, const uint32_t *tit, int pfrom, int npairs, const double *bh,
-                                          const uint32_t *tmh, const double *Mcur, int lane, float *pc32 = nullptr) {
+                                          const uint32_t *tmh, const double *Mcur, int lane) {
   #pragma unroll 1
   for (int p = pfrom + lane; p < npairs; p += 32) {
     const uint32_t e = tit[p];
@@ -315,11 +315,6 @@ __device__ __noinline__ void prefix_frame(double *pc, const uint32_t *tit, int p
     for (uint32_t bb = tmh[h] & ((1u << t) - 1u); bb; bb &= bb - 1u)
       x = torsion_apply_a(Mcur + 12 * (__ffs(bb) - 1), x);
     st3(pc + 3 * p, x);
-    if (pc32) {
-      pc32[3 * p] = (float)x.x;
-      pc32[3 * p + 1] = (float)x.y;
-      pc32[3 * p + 2] = (float)x.z;
-    }
   }
 }
 
@@ -452,7 +447,7 @@ __device__ __forceinline__ float frame_max32(const float *t32, int n, int lane) 
 #define VS_SEARCH_MINB (16 / kWarps)  // A/B only: a higher count caps the registers (96 at 10: +9% search time)
 #endif
 #ifndef VS_SCREEN_MINB
-#define VS_SCREEN_MINB 7
+#define VS_SCREEN_MINB 8
 #endif
 constexpr int kMaxWarpsSM = 24;  // warp slots per SM in the global scratch
 
@@ -499,15 +494,9 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
   double *Mcur = W + A.o_Mcur;
   double *Mvar = W + A.o_Mvar;
   float *t32 = reinterpret_cast<float *>(W + A.o_t32);
-  float *M32 = reinterpret_cast<float *>(W + A.o_M32);
-  float *kap = reinterpret_cast<float *>(W + A.o_kap);
   float *A32 = reinterpret_cast<float *>(W + A.o_A32);
   float *vc32 = reinterpret_cast<float *>(W + A.o_vc32);
-  // screen: FP32 stage-t prefixes in the warp's global scratch (read in the
-  // torsion screen, rewritten only after a torsion move)
-  float *pc32 = reinterpret_cast<float *>(hx + ((3 * (size_t)A.Nmax + 3 * (size_t)A.nmax * A.mmax + 1) & ~(size_t)1));
-  int *crow = reinterpret_cast<int *>(W + A.o_pc32);  // screen: candidate rows and item ends of a batch
-  float *s_ub = reinterpret_cast<float *>(W + A.o_vex);  // screen: upper bound of every neighbour row
+  int *crow = reinterpret_cast<int *>(W + A.o_crow);  // screen: rigid candidate rows
   const screen_grid &sg = A.p.scr;
   float Xf = 0.0f;  // screen: |frame|inf bound of the rigid items
   unsigned mgn = 1u;  // screen: ceil(2^32 / n), it / n == umulhi(it, mgn) for the rigid items
@@ -681,7 +670,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
       hydrogen_frame(hx, N, base, tm, hv, Mcur, 0xffffffffu, lane);
     }
     __syncwarp();
-    prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane, SCR ? pc32 : nullptr);
+    prefix_frame(pc, s_tit, 0, meta.d_total, s_bh, s_tmh, Mcur, lane);
     __syncwarp();
     if (SCR) Xf = frame_max32(t32, n, lane);
     // initial_poses entry point: the flat centroid of these angles
@@ -855,18 +844,6 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
         ph_acc[14] += pr_rg;
       }
 #endif
-      if (SCR && !mvar_valid) {
-        // the screen's FP32 copies of the torsion-neighbour matrices (all
-        // lanes, coalesced) and their error constants 5.75 |p~|inf
-        __syncwarp();
-        const int nm12 = 12 * m * (m + 1);
-        #pragma unroll 1
-        for (int i = lane; i < nm12; i += 32) M32[i] = (float)Mvar[i];
-        __syncwarp();
-        #pragma unroll 1
-        for (int i = lane; i < m * (m + 1); i += 32)
-          kap[i] = 5.75f * fmaxf(fmaxf(fabsf(M32[12 * i + 9]), fabsf(M32[12 * i + 10])), fabsf(M32[12 * i + 11]));
-      }
       mvar_valid = true;
       __syncwarp();
       PH(ph_rebuild ? 9 : 1)
@@ -882,7 +859,6 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
       double bv = S[S_GEO];
       int bj = -1;
       int tg = 0;  // next torsion to schedule
-      float lbmax = -__int_as_float(0x7f800000);  // screen: largest proven lower bound so far
       const float S32 = (float)bv, aS = fabsf(S32);
       for (int grp = 0; grp == 0 || tg < m; ++grp) {
         int j0, jn, tlo = 0, thi = 0, items;
@@ -898,107 +874,62 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
           jn = 2 * (thi - tlo);
           items = 2 * (s_doff[thi - 1] + s_dcnt[thi - 1] - s_doff[tlo]);
         }
+        const int *rmap = nullptr;  // screen: compact row ci -> rigid neighbour j
         if constexpr (SCR) {
-          // ---- FP32 screen of the group: per item (v~ - fl32(vcur), bound).
-          // One loop and one sampler call site for both neighbour kinds (the
-          // search is instruction-cache bound: the hot code must stay small).
-          float2 *vs2 = reinterpret_cast<float2 *>(vb);
-          {
-            const bool rig = grp == 0;
-            const uint32_t *ti = s_tit + s_doff[tlo];
-            const float *pcg = pc32 + 3 * s_doff[tlo];
-            const float cY = kU32 * 5.1f * kSqrt3 * (float)pg.inv_h * 1.0001f;
-            const float cE = kU32 * kSqrt3 * 1.01f * (float)pg.inv_h;
+          if (grp == 0) {
+            // ---- FP32 screen of the 12 rigid neighbours: per item (v~ -
+            // fl32(vcur), bound), then a proven bracket per row; only rows
+            // whose bracket reaches max(current score, best lower bound) are
+            // sampled exactly below (search.cpp:138 is decided in FP64)
+            float2 *vs2 = reinterpret_cast<float2 *>(vb);
             #pragma unroll 1
             for (int it = lane; it < items; it += 32) {
-              const float *Sj;
-              float x0, x1, x2, eacc = 0.0f;
-              int h;
-              if (rig) {
-                const int j = n == 1 ? it : (int)__umulhi((unsigned)it, mgn);
-                h = it - j * n;
-                Sj = A32 + 16 * j;
-                x0 = t32[3 * h];
-                x1 = t32[3 * h + 1];
-                x2 = t32[3 * h + 2];
-              } else {
-                // torsion item: pair (t, h in D_t) it / 2, sign it & 1, from its
-                // FP32 stage-t prefix through the variant's FP32 matrices
-                const uint32_t e = ti[it >> 1];
-                const int v = ((e >> 8) & 63) | (it & 1), t = v >> 1;
-                h = e & 255;
-                x0 = pcg[3 * (it >> 1)];
-                x1 = pcg[3 * (it >> 1) + 1];
-                x2 = pcg[3 * (it >> 1) + 2];
-                eacc = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fabsf(x2));
-                const int mb = mvar_off(v, t, m) / 12 - t;
-                #pragma unroll 1
-                for (uint32_t bb = (s_tmh[h] & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u) {
-                  const int mi = mb + __ffs(bb) - 1;
-                  const float4 q0 = *reinterpret_cast<const float4 *>(M32 + 12 * mi);
-                  const float4 q1 = *reinterpret_cast<const float4 *>(M32 + 12 * mi + 4);
-                  const float4 q2 = *reinterpret_cast<const float4 *>(M32 + 12 * mi + 8);
-                  const float d0 = x0 - q2.y, d1 = x1 - q2.z, d2 = x2 - q2.w;
-                  const float D = fmaxf(fmaxf(fabsf(d0), fabsf(d1)), fabsf(d2));
-                  x0 = fmaf(q0.z, d2, fmaf(q0.y, d1, fmaf(q0.x, d0, q2.y)));
-                  x1 = fmaf(q1.y, d2, fmaf(q1.x, d1, fmaf(q0.w, d0, q2.z)));
-                  x2 = fmaf(q2.x, d2, fmaf(q1.w, d1, fmaf(q1.z, d0, q2.w)));
-                  eacc += fmaf(8.7f, D, kap[mi]);
-                }
-                Sj = A32 + 16 * 12;
-              }
-              float lx, ly, lz;
-              screen_map(Sj, x0, x1, x2, lx, ly, lz);
-              const float Y = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fabsf(x2));
-              const float dl = rig ? Sj[12] : fmaf(cE, eacc, fmaf(cY, Y, Sj[13]));
-              float e;
-              const float val = screen_sample(sg, s_pair, lx, ly, lz, dl, e);
+              const int j = n == 1 ? it : (int)__umulhi((unsigned)it, mgn), h = it - j * n;
+              const float *Sj = A32 + 16 * j;
+              float lx, ly, lz, e;
+              screen_map(Sj, t32[3 * h], t32[3 * h + 1], t32[3 * h + 2], lx, ly, lz);
+              const float val = screen_sample(sg, s_pair, lx, ly, lz, Sj[12], e);
               vs2[it] = make_float2(val - vc32[h], e);
             }
-          }
-          __syncwarp();
-          PH(grp == 0 ? 2 : 3)
-          // ---- per-row bracket [lb, ub] of the exact geo_score
-          float ub = -__int_as_float(0x7f800000), lb = ub;
-          if (lane < jn) {
-            int base, k, stride;
-            if (grp == 0) {
-              base = lane * n;
-              k = n;
-              stride = 1;
-            } else {
-              const int t = tlo + (lane >> 1);
-              base = 2 * (s_doff[t] - s_doff[tlo]) + (lane & 1);
-              k = s_dcnt[t];
-              stride = 2;
+            __syncwarp();
+            PH(2)
+            float ub = -__int_as_float(0x7f800000), lb = ub;
+            if (lane < 12) {
+              float sd = 0.0f, sa = 0.0f, se = 0.0f;
+              #pragma unroll 4
+              for (int i = 0; i < n; ++i) {
+                const float2 q = vs2[lane * n + i];
+                sd += q.x;
+                sa += fabsf(q.x);
+                se += q.y;
+              }
+              const float st = S32 + sd;
+              const float E = fmaf(kU32, fmaf((float)(n + 2), aS + sa, sg.v3 * (float)n), se + 1e-9f) * 1.001f;
+              ub = __fadd_ru(st, E);
+              lb = __fadd_rd(st, -E);
+              if (isnan(ub) || isnan(lb)) {  // non-finite inputs: sample exactly (NaN is never adopted)
+                ub = __int_as_float(0x7f800000);
+                lb = -ub;
+              }
             }
-            float sd = 0.0f, sa = 0.0f, se = 0.0f;
-            #pragma unroll 4
-            for (int i = 0; i < k; ++i) {
-              const float2 q = vs2[base + i * stride];
-              sd += q.x;
-              sa += fabsf(q.x);
-              se += q.y;
-            }
-            const float st = S32 + sd;
-            const float E = fmaf(kU32, fmaf((float)(k + 2), aS + sa, sg.v3 * (float)k), se + 1e-9f) * 1.001f;
-            ub = __fadd_ru(st, E);
-            lb = __fadd_rd(st, -E);
-            if (isnan(ub) || isnan(lb)) {  // non-finite inputs: evaluate exactly (the reference never adopts NaN)
-              ub = __int_as_float(0x7f800000);
-              lb = -ub;
-            }
-          }
+            float gl = lb;
+            #pragma unroll
+            for (int off = 16; off > 0; off >>= 1) gl = fmaxf(gl, __shfl_xor_sync(0xffffffffu, gl, off));
+            const unsigned cand = __ballot_sync(0xffffffffu, lane < 12 && (double)ub >= fmax(bv, (double)gl));
 #ifdef VS_PHASE_PROF
-          ph_acc[17] += jn;
+            ph_acc[16] += __popc(cand);
+            ph_acc[17] += 12;
 #endif
-          float gl = lb;
-          #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) gl = fmaxf(gl, __shfl_xor_sync(0xffffffffu, gl, off));
-          lbmax = fmaxf(lbmax, gl);
-          if (lane < jn) s_ub[j0 + lane] = ub;
-          __syncwarp();
-          continue;
+            if (!cand) {
+              PH(4)
+              continue;  // no rigid neighbour can beat the current pose or another's lower bound
+            }
+            if ((cand >> lane) & 1u) crow[__popc(cand & ((1u << lane) - 1u))] = lane;
+            __syncwarp();
+            jn = __popc(cand);
+            items = jn * n;
+            rmap = crow;
+          }
         }
         // Rigid and torsion neighbours run in separate compact loops, one
         // sample in flight per lane: the search is instruction-fetch bound
@@ -1032,9 +963,10 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
               h = rh;
               row = rj;
               col = s_hl[h];
-              R = rj < 6 ? S + S_R : Rj + kRow * (rj - 6);
-              T = rj < 6 ? Tj + 4 * rj : R + 10;
-              x = ld3(TORSH(h, col));
+              const int jr = rmap ? rmap[rj] : rj;
+              R = jr < 6 ? S + S_R : Rj + kRow * (jr - 6);
+              T = jr < 6 ? Tj + 4 * jr : R + 10;
+              x = ld3(SCR ? hx + 3 * col : TORSH(h, col));
               rh += 32;
               #pragma unroll 1
               while (rh >= n) {
@@ -1113,7 +1045,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
         }
         if (gv > bv) {  // search.cpp:138: strictly better than everything before
           bv = gv;
-          bj = j0 + gj;
+          bj = j0 + (rmap ? rmap[gj] : gj);
           const double *row = vb + gj * nmax;
 #if VS_ROW_SELECT
           const uint32_t tb = grp != 0 ? 1u << (tlo + (gj >> 1)) : 0xffffffffu;
@@ -1125,120 +1057,6 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
 #endif
         }
         __syncwarp();
-        PH(4)
-      }
-      if constexpr (SCR) {
-        // ---- exact FP64 evaluation of every neighbour whose bracket reaches
-        // tau = max(current score, largest lower bound): in neighbour order,
-        // batches of <= kGroup rows in one flattened pass (rows into vb)
-        const double tau = fmax(bv, (double)lbmax);
-        #pragma unroll 1
-        for (int J0 = 0; J0 < J; J0 += 32) {
-          unsigned cand = __ballot_sync(0xffffffffu, J0 + lane < J && (double)s_ub[J0 + lane] >= tau);
-          #pragma unroll 1
-          while (cand) {
-            unsigned batch = cand;
-            if (__popc(batch) > kGroup) batch &= (1u << (__fns(batch, 0, kGroup + 1))) - 1u;
-            cand &= ~batch;
-            const int K = __popc(batch);
-            int cnt = 0;
-            if ((batch >> lane) & 1u) {
-              const int ci = __popc(batch & ((1u << lane) - 1u));
-              const int row = J0 + lane;
-              crow[ci] = row;
-              cnt = row < 12 ? n : s_dcnt[(row - 12) >> 1];
-            }
-            int incl = cnt;  // inclusive scan of the item counts in row order
-            #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-              const int o = __shfl_up_sync(0xffffffffu, incl, off);
-              if (lane >= off) incl += o;
-            }
-            const int total = __shfl_sync(0xffffffffu, incl, 31);
-            if ((batch >> lane) & 1u) crow[kGroup + __popc(batch & ((1u << lane) - 1u))] = incl;
-            __syncwarp();
-#ifdef VS_PHASE_PROF
-            ph_acc[16] += K;
-#endif
-            double *vx = vb;  // K rows of nmax doubles
-            #pragma unroll 1
-            for (int it = lane; it < total; it += 32) {
-              int ci = 0, first = 0;
-              #pragma unroll 1
-              for (int c = 0; c < K; ++c) {
-                const int end = crow[kGroup + c];
-                if (it < end) {
-                  ci = c;
-                  break;
-                }
-                first = end;
-              }
-              const int row = crow[ci], i = it - first;
-              const double *R = S + S_R, *T = S + S_T;
-              int h, col;
-              d3 x;
-              if (row < 12) {
-                if (row >= 6) {
-                  R = Rj + kRow * (row - 6);
-                  T = R + 10;
-                } else {
-                  T = Tj + 4 * row;
-                }
-                h = i;
-                col = s_hl[i];
-                x = ld3(hx + 3 * col);
-              } else {
-                const int v = row - 12, t = v >> 1;
-                const double *Mv = Mvar + mvar_off(v, t, m) - 12 * t;
-                const int pp = s_doff[t] + i;
-                h = s_tit[pp] & 255;
-                x = ld3(pc + 3 * pp);
-                const uint32_t mask = s_tmh[h];
-                col = (int)(mask >> 31);
-                #pragma unroll 1
-                for (uint32_t bb = (mask & 0x7fffffffu) >> t << t; bb; bb &= bb - 1u)
-                  x = torsion_apply_a(Mv + 12 * (__ffs(bb) - 1), x);
-              }
-              bool out;
-              vx[ci * nmax + h] = field_value_fast<MODE>(g, pg, pal, rigid_col_rt(R, T, x, col), out);
-            }
-            __syncwarp();
-            // geo_score of each candidate: the reference's sequential sum in
-            // heavy-atom order (grid.cpp:97-101), atoms outside D_t from the
-            // current pose; then the first strict maximum (search.cpp:138)
-            double acc = -__longlong_as_double(0x7ff0000000000000LL);
-            int rr = 0x7fffffff, ci = lane;
-            if (lane < K) {
-              rr = crow[lane];
-              const double *rw = vx + lane * nmax;
-              const uint32_t tb = rr < 12 ? 0xffffffffu : 1u << ((rr - 12) >> 1);
-              double a = 0.0;
-              #pragma unroll 4
-              for (int h = 0; h < n; ++h) a += (rr < 12 || (s_dm[h] & tb)) ? rw[h] : vcur[h];
-              acc = isnan(a) ? acc : a;
-            }
-            #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              const double ov = __shfl_xor_sync(0xffffffffu, acc, off);
-              const int orr = __shfl_xor_sync(0xffffffffu, rr, off);
-              const int oci = __shfl_xor_sync(0xffffffffu, ci, off);
-              if (ov > acc || (ov == acc && orr < rr)) {
-                acc = ov;
-                rr = orr;
-                ci = oci;
-              }
-            }
-            if (acc > bv) {
-              bv = acc;
-              bj = rr;
-              const double *rw = vx + ci * nmax;
-              const uint32_t tb = rr < 12 ? 0xffffffffu : 1u << ((rr - 12) >> 1);
-              #pragma unroll 1
-              for (int h = lane; h < n; h += 32) vbest[h] = (rr < 12 || (s_dm[h] & tb)) ? rw[h] : vcur[h];
-            }
-            __syncwarp();
-          }
-        }
         PH(4)
       }
       evals += (unsigned long long)n * J;
@@ -1296,7 +1114,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
             st3(hx + 3 * s_hl[h], x);
           }
           hydrogen_frame(hx, N, base, tm, hv, Mcur, dep, lane);
-          prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane, SCR ? pc32 : nullptr);
+          prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane);
           if (SCR) {
             __syncwarp();
             Xf = frame_max32(t32, n, lane);
@@ -1365,7 +1183,7 @@ namespace {
 
 struct Layout {
   int o_tors, o_Mcur, o_Mvar, o_Rj, o_vb, o_vbest, o_vcur, o_cache, o_ang, o_sccur, o_state, o_ints, total;
-  int o_t32, o_M32, o_kap, o_A32, o_vex, o_vc32, o_pc32;
+  int o_t32, o_A32, o_vc32, o_crow;
   int cta;  // CTA-shared ligand staging, doubles
 };
 
@@ -1392,24 +1210,18 @@ Layout layout(int Nm, int nm, int mm, int dm, bool scr) {
   L.o_state = take(S_N);
   L.o_ints = take((2 * mm + 1) / 2 + 1);
   if (scr) {
-    L.o_t32 = take((3 * nm + 1) / 2);
-    L.o_M32 = take(6 * mm * (mm + 1));     // 12 floats per matrix
-    L.o_kap = take((mm * (mm + 1) + 1) / 2);
-    L.o_A32 = take(13 * 8);               // 13 slots x 16 floats
-    L.o_vex = take((12 + 2 * mm + 1) / 2);  // row upper bounds (floats)
-    L.o_vc32 = take((nm + 1) / 2);
-    L.o_pc32 = take(kGroup);  // candidate rows and their item ends (ints)
+    L.o_t32 = take((3 * nm + 1) / 2);  // FP32 heavy-atom frame
+    L.o_A32 = take(13 * 8);            // 13 FP32 rigid maps x 16 floats
+    L.o_vc32 = take((nm + 1) / 2);     // FP32 current samples
+    L.o_crow = take(6);                // candidate rows (12 ints)
   }
   L.total = o;
   return L;
 }
 
-// Global scratch per warp, in doubles: hydrogen frame (3 Nmax), stage-t
-// prefixes (3 nmax mmax) and their FP32 copies (screen), 16-byte aligned.
-size_t scr_stride(int Nm, int nm, int mm) {
-  const size_t pre = (3 * (size_t)Nm + 3 * (size_t)nm * mm + 1) & ~(size_t)1;
-  return pre + ((3 * (size_t)nm * mm + 3) / 2 & ~(size_t)1) + 2;
-}
+// Global scratch per warp, in doubles: hydrogen frame (3 Nmax) and stage-t
+// prefixes (3 nmax mmax), 16-byte aligned.
+size_t scr_stride(int Nm, int nm, int mm) { return (3 * (size_t)Nm + 3 * (size_t)nm * mm + 1) & ~(size_t)1; }
 
 bool use_screen(const search_args &A) { return A.pg.mode == 1 && A.p.scr.w != nullptr; }
 
@@ -1430,12 +1242,9 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
   A.o_state = L.o_state;
   A.o_ints = L.o_ints;
   A.o_t32 = L.o_t32;
-  A.o_M32 = L.o_M32;
-  A.o_kap = L.o_kap;
   A.o_A32 = L.o_A32;
-  A.o_vex = L.o_vex;
   A.o_vc32 = L.o_vc32;
-  A.o_pc32 = L.o_pc32;
+  A.o_crow = L.o_crow;
   A.warp_doubles = L.total;
   A.scr_stride = scr_stride(A.Nmax, A.nmax, A.mmax);
   const int o = L.total;
