@@ -26,6 +26,9 @@ from paper_2110_11644_b200.model import LigandBatch  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--per-cell", type=int, default=20000)
+    ap.add_argument("--distinct", type=int, default=8192,
+                    help="distinct ligands generated per cell (generated on all host threads); the cell's batch "
+                         "repeats them up to --per-cell (every copy is docked again)")
     ap.add_argument("--cpu-sample", type=int, default=64)
     ap.add_argument("--heavy", default="10,20,30,40,50,60,70,80")
     ap.add_argument("--rot", default="0,3,6,9,12,15")
@@ -47,21 +50,35 @@ def main():
     for n in [int(x) for x in args.heavy.split(",")]:
         for m in [int(x) for x in args.rot.split(",")]:
             cell = {"heavy": n, "rotors": m}
+            distinct = min(args.distinct, args.per_cell)
             try:
-                smi = api.synthetic_smiles(args.per_cell, seed=20260819 + 1000 * n + m, heavy=(max(1, n - 2), n + 2),
-                                           rot=(m, m), grammar=args.grammar)
+                api.synthetic_smiles(1, seed=20260819 + 1000 * n + m, heavy=(max(1, n - 2), n + 2), rot=(m, m),
+                                     grammar=args.grammar)
             except ValueError:
                 print(json.dumps({**cell, "skipped": "generator cannot reach this (heavy, rotor) window"}), flush=True)
                 continue
+            # rejection sampling into narrow windows is slow: chunks of 512
+            # with derived seeds on all host threads (ctypes releases the GIL)
+            from concurrent.futures import ThreadPoolExecutor
+            chunks = [(i, min(512, distinct - i)) for i in range(0, distinct, 512)]
+            t_gen = time.perf_counter()
+            with ThreadPoolExecutor(threads) as ex:
+                parts = list(ex.map(lambda c: api.synthetic_smiles(
+                    c[1], seed=20260819 + 1000 * n + m + 7919 * (c[0] // 512), heavy=(max(1, n - 2), n + 2),
+                    rot=(m, m), grammar=args.grammar), chunks))
+            gen_s = time.perf_counter() - t_gen
+            uniq = [x for p in parts for x in p]
+            smi = (uniq * (args.per_cell // len(uniq) + 1))[:args.per_cell]
             t0 = time.perf_counter()
-            ligs = api.prepare_ligand(smi, quantize=True, ctx=ctx, nthreads=threads)
+            ul = api.prepare_ligand(uniq, quantize=True, ctx=ctx, nthreads=threads)
+            ligs = (ul * (args.per_cell // len(ul) + 1))[:args.per_cell]
             prep_s = time.perf_counter() - t0
             batch = LigandBatch(ligs)
             api.dock_and_score_batch(pocket, LigandBatch(ligs[:2048]), cfg, ctx, want_conformation=False)  # warm-up
             r = api.dock_and_score_batch(pocket, batch, cfg, ctx, want_conformation=False)
             line = {**cell, "ligands": len(ligs), "gpu_ligands_per_s": len(ligs) / (r.kernel_ms / 1e3),
                     "stage_ms": {k: round(v, 2) for k, v in r.stage_ms.items()},
-                    "ok": int((r.results["status"] == 0).sum()), "host_prep_s": round(prep_s, 2),
+                    "ok": int((r.results["status"] == 0).sum()), "host_prep_s": round(prep_s, 2), "distinct": len(uniq), "smiles_gen_s": round(gen_s, 1),
                     "mean_atoms": float(batch.n_atoms_total / max(batch.n_ligands, 1))}
             if ref is not None and args.cpu_sample > 0:
                 sample = LigandBatch(ligs[:args.cpu_sample])
