@@ -14,7 +14,9 @@ for f in kernels search driver peaks codec; do
 done
 g++ -std=c++17 -O2 -fPIC -ffp-contract=off -fno-fast-math -Wall -I../../include -c host/prep.cpp -o $OBJ/prep.o & pids+=($!)
 g++ -std=c++17 -O2 -fPIC -ffp-contract=off -fno-fast-math -Wall -I../../include -c host/synth.cpp -o $OBJ/synth.o & pids+=($!)
+g++ -std=c++17 -O2 -fPIC -ffp-contract=off -fno-fast-math -Wall -pthread -I../../include -c host/rank.cpp -o $OBJ/rank.o & pids+=($!)
+g++ -std=c++17 -O2 -fPIC -ffp-contract=off -fno-fast-math -Wall -pthread -I../../include -c host/merge.cpp -o $OBJ/merge.o & pids+=($!)
 for p in "${pids[@]}"; do wait $p || { echo "variant $NAME: compile failed"; exit 1; }; done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../_lib/var/$NAME.so \
-  $OBJ/kernels.o $OBJ/search.o $OBJ/driver.o $OBJ/peaks.o $OBJ/codec.o $OBJ/prep.o $OBJ/synth.o -lpthread
+  $OBJ/kernels.o $OBJ/search.o $OBJ/driver.o $OBJ/peaks.o $OBJ/codec.o $OBJ/prep.o $OBJ/synth.o $OBJ/rank.o $OBJ/merge.o -lpthread
 echo "built _lib/var/$NAME.so"

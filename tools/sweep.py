@@ -57,17 +57,30 @@ def main():
             except ValueError:
                 print(json.dumps({**cell, "skipped": "generator cannot reach this (heavy, rotor) window"}), flush=True)
                 continue
-            # rejection sampling into narrow windows is slow: chunks of 512
-            # with derived seeds on all host threads (ctypes releases the GIL)
+            # rejection sampling into narrow windows is slow: chunks of 256 (one
+            # generator block) with derived seeds on all host threads (ctypes
+            # releases the GIL); a chunk the generator gives up on is retried
+            # with the next seed
             from concurrent.futures import ThreadPoolExecutor
-            chunks = [(i, min(512, distinct - i)) for i in range(0, distinct, 512)]
+
+            def chunk(i):
+                try:
+                    return api.synthetic_smiles(256, seed=20260819 + 1000 * n + m + 7919 * i,
+                                                heavy=(max(1, n - 2), n + 2), rot=(m, m), grammar=args.grammar)
+                except ValueError:
+                    return []
             t_gen = time.perf_counter()
+            parts, i0 = [], 0
             with ThreadPoolExecutor(threads) as ex:
-                parts = list(ex.map(lambda c: api.synthetic_smiles(
-                    c[1], seed=20260819 + 1000 * n + m + 7919 * (c[0] // 512), heavy=(max(1, n - 2), n + 2),
-                    rot=(m, m), grammar=args.grammar), chunks))
+                while sum(len(p) for p in parts) < distinct and i0 < 8 * (distinct // 256 + 1):
+                    k = threads
+                    parts += list(ex.map(chunk, range(i0, i0 + k)))
+                    i0 += k
             gen_s = time.perf_counter() - t_gen
-            uniq = [x for p in parts for x in p]
+            if not any(parts):
+                print(json.dumps({**cell, "skipped": "generator cannot reach this (heavy, rotor) window"}), flush=True)
+                continue
+            uniq = [x for p in parts for x in p][:distinct]
             smi = (uniq * (args.per_cell // len(uniq) + 1))[:args.per_cell]
             t0 = time.perf_counter()
             ul = api.prepare_ligand(uniq, quantize=True, ctx=ctx, nthreads=threads)
