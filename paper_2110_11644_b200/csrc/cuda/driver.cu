@@ -641,19 +641,12 @@ std::vector<int> chunks(const vs_ligand_batch *b, int k, size_t budget) {
   return cut;
 }
 
-// Per-restart outputs of the search.  fused: one slot of k restarts per
-// search CTA (the select runs inside the search kernel, so the slots are
-// reused ligand after ligand and stay L2-resident); else k restarts per
-// ligand of the batch.
-vs_status ensure_items(vs_context *ctx, const Staged &st, int k, vsd::item_out &o, bool fused = false) {
-  const size_t slots = fused ? static_cast<size_t>(vsd::search_max_ctas(ctx->num_sms)) : 0;
-  const size_t items = (fused ? slots : static_cast<size_t>(std::max(st.n, 1))) * k;
-  const size_t angs = fused ? items * std::max(st.mmax, 1) : std::max<size_t>(1, static_cast<size_t>(st.torsions) * k);
-  const size_t confs = fused ? items * std::max(st.Nmax, 1) : std::max<size_t>(1, static_cast<size_t>(st.atoms) * k);
+vs_status ensure_items(vs_context *ctx, const Staged &st, int k, vsd::item_out &o) {
+  const size_t items = static_cast<size_t>(std::max(st.n, 1)) * k;
   CUDA_TRY(ctx->out_geo.ensure(sizeof(double) * items));
   CUDA_TRY(ctx->out_T.ensure(sizeof(double) * 7 * items));
-  CUDA_TRY(ctx->out_ang.ensure(sizeof(double) * angs));
-  CUDA_TRY(ctx->out_conf.ensure(sizeof(double) * 3 * confs));
+  CUDA_TRY(ctx->out_ang.ensure(sizeof(double) * std::max<size_t>(1, static_cast<size_t>(st.torsions) * k)));
+  CUDA_TRY(ctx->out_conf.ensure(sizeof(double) * 3 * std::max<size_t>(1, static_cast<size_t>(st.atoms) * k)));
   CUDA_TRY(ctx->out_evals.ensure(sizeof(unsigned long long) * items));
   CUDA_TRY(ctx->out_status.ensure(sizeof(int) * items));
   CUDA_TRY(ctx->out_iters.ensure(sizeof(int) * items));
@@ -929,11 +922,8 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
     if (!pre && (rc = stage(ctx, batch, l0, l1, st))) return rc;
     vsd::flat_out f{};
     vsd::item_out o{};
-    // the select runs in the search kernel's epilogue (one warp per ligand,
-    // k <= 32); VS_NO_FUSED_SELECT=1 keeps the separate k_select_warp (A/B)
-    const bool fused = k <= 32 && std::getenv("VS_NO_FUSED_SELECT") == nullptr;
     if ((rc = ensure_flat(ctx, st, f))) return rc;
-    if ((rc = ensure_items(ctx, st, k, o, fused))) return rc;
+    if ((rc = ensure_items(ctx, st, k, o))) return rc;
     CUDA_TRY(ctx->results.ensure(sizeof(vs_dock_result) * std::max(st.n, 1)));
     CUDA_TRY(ctx->best_ang.ensure(sizeof(double) * std::max(st.torsions, 1)));
     CUDA_TRY(ctx->best_conf.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
@@ -1001,15 +991,15 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
         CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
         CUDA_TRY(vsd::launch_search(st.b, pd, sc, f, o, ctx->work.as<int>(), Nm, nm, mm, ctx->num_sms, ctx->stream,
                                     nullptr, ctx->search_args.p, ctx->lig_index.as<int>() + ranges[bi].first,
-                                    ranges[bi].second, dm, fused ? &d : nullptr));
+                                    ranges[bi].second, dm));
         ++ctx->last_launches;
       }
       --ctx->last_launches;  // counted once below with the fixed launches
     }
     CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
-    if (!fused) CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
+    CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));
-    ctx->last_launches += (pi == 0 ? 4 : 2) - (fused ? 1 : 0);
+    ctx->last_launches += pi == 0 ? 4 : 2;
     CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,
                              ctx->stream));
     const int T0 = batch ? batch->torsion_offset[l0] : 0, A0 = batch ? batch->atom_offset[l0] : 0;

@@ -136,10 +136,7 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf,
-                          const int *lig_index = nullptr, int n_lig = 0, int dmax = 0,
-                          const dock_out *fused_select = nullptr);
-// CTAs a search launch may use (the fused select's per-CTA restart slots)
-int search_max_ctas(int num_sms);
+                          const int *lig_index = nullptr, int n_lig = 0, int dmax = 0);
 // device buffer size the search launchers need for their argument block
 cudaError_t launch_decode(const uint8_t *bytes, const int64_t *offs, int n, const int *atom_off, const int *bond_off,
                           const int *tors_off, const int64_t *rs_off, double *xyz, uint8_t *elem, uint8_t *heavy,

@@ -31,7 +31,6 @@
 #include "../../../include/vs_crtrig.h"
 #include "../../../include/vs_dock.h"
 #include "kernels.cuh"
-#include "select.cuh"
 
 namespace vsd {
 
@@ -194,12 +193,6 @@ struct search_args {
   // candidate row, FP32 current samples, FP32 stage-t prefixes
   int o_t32, o_A32, o_vc32, o_crow;
   size_t scr_stride;     // doubles of global scratch per warp
-  // fused select (dock path, k <= 32): the restarts of a ligand are items
-  // blockIdx.x * k + r of `o` (a per-CTA slot, L2-resident, instead of one
-  // DRAM-sized array over the batch) and warp 0 runs cluster_and_select +
-  // chem_score + the best pose (select.cuh) when the ligand's restarts are done
-  int fused;
-  dock_out d;
 };
 
 // Offset (in doubles) of variant v's matrix for torsion u >= t(v) inside the
@@ -540,14 +533,9 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
     if (li >= A.n_lig) break;
     const int l = A.lig_index ? A.lig_index[li] : li;
     const lig_meta meta = b.meta[l];
-    // this ligand's restarts in `o`: per-CTA slot when the select is fused
-    const size_t item0 = A.fused ? (size_t)blockIdx.x * k : (size_t)l * k;
     if (meta.status != VS_LIG_OK) {
       #pragma unroll 1
-      for (int r = threadIdx.x; r < k; r += blockDim.x) A.o.status[item0 + r] = meta.status;
-      if (A.fused && warp == 0)  // the rejected ligand's result: status only
-        select_ligand_warp(b, A.p, A.c, A.o, item0, A.o.conf, 0, A.d, l, lane, reinterpret_cast<int *>(W + A.o_vb),
-                           reinterpret_cast<int *>(W + A.o_vb) + 32, reinterpret_cast<int *>(W + A.o_vb) + 64);
+      for (int r = threadIdx.x; r < k; r += blockDim.x) A.o.status[l * k + r] = meta.status;
       continue;
     }
     const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
@@ -607,7 +595,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
     if (lane == 0) r = atomicAdd(&sh_r, 1);
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= k) break;
-    const size_t item = item0 + r;  // item index of the outputs
+    const int item = l * k + r;  // global item index of the outputs
     unsigned long long evals = 0;
 
     // ---- per-restart tables
@@ -1163,14 +1151,14 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
     }
     // ---- outputs: the pose's conformation = apply_rigid(tors, T); in
     // local_search mode an unmoved pose returns its input conformation.
-    const size_t ck = A.fused ? 3 * ((size_t)blockIdx.x * k * A.Nmax + (size_t)r * N) : 3 * ((size_t)a0 * k + (size_t)r * N);
+    const size_t ck = 3 * ((size_t)a0 * k + (size_t)r * N);
     if (ls_mode && !moved) {
       #pragma unroll 1
       for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
     } else {
       full_conformation(A.o.conf + ck, S, N, hx, true, lane);
     }
-    const size_t tk = A.fused ? (size_t)blockIdx.x * k * A.mmax + (size_t)r * m : (size_t)t0 * k + (size_t)r * m;
+    const size_t tk = (size_t)t0 * k + (size_t)r * m;
     #pragma unroll 1
     for (int u = lane; u < m; u += 32) A.o.ang[tk + u] = ang[u];
     if (lane < 4)
@@ -1187,16 +1175,6 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
     __syncwarp();
     PH(8)
   }  // restarts
-    if (A.fused) {
-      // cluster_and_select + chem_score + best (search.cpp:195-275) of this
-      // ligand from the CTA's slot, while the slot is still in L2
-      __syncthreads();
-      if (warp == 0) {
-        int *ws = reinterpret_cast<int *>(W + A.o_vb);
-        select_ligand_warp(b, A.p, A.c, A.o, item0, A.o.conf + 3 * (size_t)blockIdx.x * k * A.Nmax,
-                           (size_t)blockIdx.x * k * A.mmax, A.d, l, lane, ws, ws + 32, ws + 64);
-      }
-    }
   }  // ligands
   PH_FLUSH
 }
@@ -1338,17 +1316,11 @@ size_t search_smem_bytes(int N, int n, int m, int dtot, bool screen) {
   return (size_t)(kPalDoubles + L.cta + L.total * kWarps) * sizeof(double) + (screen ? 128 : 0);
 }
 
-int search_max_ctas(int num_sms) { return num_sms * (kMaxWarpsSM / kWarps); }
-
 cudaError_t launch_search(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const flat_out &f,
                           const item_out &o, int *work_counter, int nmax_atoms, int nmax_heavy, int mmax,
                           int num_sms, cudaStream_t s, int *launches, void *args_buf, const int *lig_index,
-                          int n_lig, int dmax, const dock_out *fused) {
+                          int n_lig, int dmax) {
   search_args A{};
-  if (fused) {
-    A.fused = 1;
-    A.d = *fused;
-  }
   A.hscr = static_cast<double *>(args_buf);
   A.scr_warps = num_sms * kMaxWarpsSM;
   A.b = b;
