@@ -5,6 +5,7 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "vscreen/b200/prepare.hpp"
@@ -203,6 +204,30 @@ int main() {
     CHECK(sink.data() == want);
     CHECK(rs.rows_written == 3 && rs.ligands_docked == 3 && rs.records_skipped == 0 && rs.dock_errors == 0);
     CHECK(plan_slabs(10, 3)[1].slab_start == 3 && plan_slabs(10, 3)[2].slab_stop == 10);
+    // file source / sink and merge_outputs (pipeline.cpp:391-412): two slabs
+    // written to rank files, concatenated, equal the one-slab output
+    const std::string dir = "/tmp/vs_dropin_rank";
+    std::system(("mkdir -p " + dir).c_str());
+    {
+      std::FILE *f = std::fopen((dir + "/lib.xslb").c_str(), "wb");
+      std::fwrite(img.data(), 1, img.size(), f);
+      std::fclose(f);
+    }
+    const std::vector<RankPlan> plans = plan_slabs(img.size(), 2);
+    std::vector<std::string> outs;
+    for (RankPlan rp : plans) {
+      rp.input_path = dir + "/lib.xslb";
+      rp.output_path = dir + "/rank" + std::to_string(rp.rank) + ".scores";
+      run_rank(rp, twin, pc);
+      outs.push_back(rp.output_path);
+    }
+    merge_outputs(outs, dir + "/merged.tsv");
+    std::FILE *mf = std::fopen((dir + "/merged.tsv").c_str(), "rb");
+    std::string merged;
+    char buf[4096];
+    for (size_t got; (got = std::fread(buf, 1, sizeof buf, mf)) > 0;) merged.append(buf, got);
+    std::fclose(mf);
+    CHECK(merged == want);
   }
 
   // per-thread device selection

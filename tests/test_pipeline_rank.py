@@ -121,3 +121,17 @@ def test_gpu_rank_corrupt_tail_fails_like_reference(gpu_ctx, setup):
         ref.run_rank(bad, pocket, cfg)
     with pytest.raises(ValueError, match="corrupt record stream"):
         api.run_rank(bad, pocket, cfg, devices=[0])
+
+
+@pytest.mark.gpu
+def test_gpu_rank_over_two_devices(gpu_ctx, setup):
+    """The CUDA workers of one rank spread over two GPUs (W per device); rows
+    and counters are unchanged (skipped on a one-GPU box)."""
+    from paper_2110_11644_b200 import native
+    if native.lib().vs_device_count() < 2:
+        pytest.skip("needs two GPUs")
+    ref, pocket, data, cfg = setup
+    want, wc = ref.run_rank(data, pocket, cfg)
+    got, st = api.run_rank(data, pocket, cfg, devices=[0, 1], batch_records=6, workers_per_device=2)
+    assert got == want and st["workers"] == 4
+    assert st["rows_written"] == wc["rows_written"] and st["records_skipped"] == wc["records_skipped"]
