@@ -207,7 +207,7 @@ int main() {
     // file source / sink and merge_outputs (pipeline.cpp:391-412): two slabs
     // written to rank files, concatenated, equal the one-slab output
     const std::string dir = "/tmp/vs_dropin_rank";
-    std::system(("mkdir -p " + dir).c_str());
+    if (std::system(("mkdir -p " + dir).c_str()) != 0) ++failures;
     {
       std::FILE *f = std::fopen((dir + "/lib.xslb").c_str(), "wb");
       std::fwrite(img.data(), 1, img.size(), f);
