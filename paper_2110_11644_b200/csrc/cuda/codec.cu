@@ -209,6 +209,12 @@ cudaError_t launch_decode(const uint8_t *bytes, const int64_t *offs, int n, cons
   return cudaGetLastError();
 }
 
+void preload_kernels_codec() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_decode);
+  cudaFuncGetAttributes(&a, k_compact_right);
+}
+
 }  // namespace vsd
 
 // ------------------------------------------------------------------ host

@@ -746,6 +746,18 @@ vs_status vs_context_create(int device, vs_context **out) {
   for (auto &e : ctx->evs) cudaEventCreate(&e);
   cudaEventCreate(&ctx->ev_flat);
   ensure_lattice(device);
+  {
+    // eager module load per device, once per process: concurrent first
+    // launches from several host threads on a fresh device (the rank's CUDA
+    // workers) raced inside CUDA's lazy loading
+    static std::mutex mu;
+    static bool loaded[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (!loaded[device & 63]) {
+      vsd::preload_kernels();
+      loaded[device & 63] = true;
+    }
+  }
   *out = ctx;
   return VS_OK;
 }

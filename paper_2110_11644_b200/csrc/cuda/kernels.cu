@@ -1333,4 +1333,25 @@ cudaError_t launch_build_pocket(const double *hxyz, int nh, double cx, double cy
   return cudaGetLastError();
 }
 
+// Load this translation unit's kernels on the current device (CUDA lazy
+// loading would otherwise load them at first launch, and concurrent first
+// launches from several host threads on a new device raced in
+// cudaFuncSetAttribute: "invalid argument").
+void preload_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_setup);
+  cudaFuncGetAttributes(&a, k_flatten);
+  cudaFuncGetAttributes(&a, k_flatten_dep);
+  cudaFuncGetAttributes(&a, k_select);
+  cudaFuncGetAttributes(&a, k_select_warp);
+  cudaFuncGetAttributes(&a, k_cluster);
+  cudaFuncGetAttributes(&a, k_field);
+  cudaFuncGetAttributes(&a, k_geo);
+  cudaFuncGetAttributes(&a, k_chem);
+  cudaFuncGetAttributes(&a, k_build_pocket);
+  preload_kernels_search();
+  preload_kernels_codec();
+}
+
 }  // namespace vsd
+

@@ -128,6 +128,10 @@ struct dock_out {
 };
 
 void set_lattice_table(const double *sc72, const double *lo72);
+// load every kernel of the library on the current device (vs_context_create)
+void preload_kernels();
+void preload_kernels_search();
+void preload_kernels_codec();
 void set_lattice_table_search(const double *sc72, const double *lo72);
 
 cudaError_t launch_setup(const batch_dev &b, int restarts, cudaStream_t s);

@@ -1388,4 +1388,13 @@ cudaError_t launch_local_search(const batch_dev &b, const pocket_dev &p, const s
   return run_search(A, num_sms, s, nullptr);
 }
 
+void preload_kernels_search() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_search<0, false>);
+  cudaFuncGetAttributes(&a, k_search<1, false>);
+  cudaFuncGetAttributes(&a, k_search<2, false>);
+  cudaFuncGetAttributes(&a, k_search<1, true>);
+}
+
 }  // namespace vsd
+
