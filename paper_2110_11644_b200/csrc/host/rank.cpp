@@ -175,6 +175,8 @@ extern "C" vs_status vs_run_rank(uint64_t source_size, vs_read_fn read, void *re
 
   // ---- CUDA workers: W per device, each with its own context and pocket copy
   std::vector<int> devs;
+  if (cf.devices && cf.n_devices <= 0)
+    return vs_internal_fail(VS_ERR_INVALID_ARGUMENT, "a device list needs n_devices > 0");
   const int ndev = cf.n_devices > 0 ? cf.n_devices : vs_device_count();
   if (ndev <= 0) return vs_internal_fail(VS_ERR_NO_DEVICE, "no CUDA device");
   for (int i = 0; i < ndev; ++i) devs.push_back(cf.devices ? cf.devices[i] : i);
