@@ -224,9 +224,9 @@ def measure_gather(device: int) -> dict:
 
 def traffic_per_launch(n_ligands: int):
     """DRAM bytes of the search stage for one step: the per-ligand figure of
-    the committed ncu capture (profiles/r01_traffic.json, dram__bytes_read +
+    the committed ncu capture (profiles/r02_traffic.json, dram__bytes_read +
     dram__bytes_write of one k_search launch) times the step's ligands."""
-    path = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
         with open(path) as f:
             return float(json.load(f)["dram_bytes_per_ligand"]) * n_ligands
