@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "vscreen/dockengine/pose.hpp"
@@ -91,6 +92,12 @@ struct RankStats {
 std::vector<RankPlan> plan_slabs(std::uint64_t file_size, int n_ranks);
 // pipeline.cpp:47-62: "SMILES\t<score, fixed 4 decimals>\n"; InvalidArgument if non-finite
 std::string format_row(const OutputRow &row);
+
+// pipeline.cpp:430-505: the rank's .stats file, one `key=value` line per
+// RankStats field (counts as integers, seconds fixed with 6 decimals);
+// parse_rank_stats throws ParseError on a malformed line or unknown key.
+std::string format_rank_stats(const RankStats &stats);
+RankStats parse_rank_stats(std::string_view text);
 
 // pipeline.cpp:297-389 / 391-396 on the B200 CUDA workers
 RankStats run_rank(const RankPlan &plan, ByteSource &source, Sink &sink, const Pocket &pocket,

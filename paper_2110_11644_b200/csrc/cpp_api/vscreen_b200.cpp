@@ -737,6 +737,93 @@ std::string format_row(const OutputRow &row) {
 }
 
 namespace {
+// RankStats fields in the .stats file's order: (key, integer member or
+// seconds member)
+struct StatField {
+  const char *key;
+  std::uint64_t RankStats::*u64;
+  double RankStats::*sec;
+  int RankStats::*i32;
+  std::size_t RankStats::*sz;
+};
+const StatField kStatFields[] = {
+    {"ligands_docked", &RankStats::ligands_docked, nullptr, nullptr, nullptr},
+    {"records_skipped", &RankStats::records_skipped, nullptr, nullptr, nullptr},
+    {"dock_errors", &RankStats::dock_errors, nullptr, nullptr, nullptr},
+    {"rows_written", &RankStats::rows_written, nullptr, nullptr, nullptr},
+    {"chunks_read", &RankStats::chunks_read, nullptr, nullptr, nullptr},
+    {"bytes_read", &RankStats::bytes_read, nullptr, nullptr, nullptr},
+    {"write_calls", &RankStats::write_calls, nullptr, nullptr, nullptr},
+    {"bytes_written", &RankStats::bytes_written, nullptr, nullptr, nullptr},
+    {"workers", nullptr, nullptr, &RankStats::workers, nullptr},
+    {"wall_seconds", nullptr, &RankStats::wall_seconds, nullptr, nullptr},
+    {"reader_busy_seconds", nullptr, &RankStats::reader_busy_seconds, nullptr, nullptr},
+    {"splitter_busy_seconds", nullptr, &RankStats::splitter_busy_seconds, nullptr, nullptr},
+    {"docker_busy_seconds", nullptr, &RankStats::docker_busy_seconds, nullptr, nullptr},
+    {"writer_busy_seconds", nullptr, &RankStats::writer_busy_seconds, nullptr, nullptr},
+    {"chunk_queue_high_water", nullptr, nullptr, nullptr, &RankStats::chunk_queue_high_water},
+    {"item_queue_high_water", nullptr, nullptr, nullptr, &RankStats::item_queue_high_water},
+    {"row_queue_high_water", nullptr, nullptr, nullptr, &RankStats::row_queue_high_water},
+};
+}  // namespace
+
+std::string format_rank_stats(const RankStats &st) {
+  std::string out;
+  for (const StatField &f : kStatFields) {
+    out += f.key;
+    out += '=';
+    if (f.sec) {
+      char buf[64];
+      const auto r = std::to_chars(buf, buf + sizeof buf, st.*f.sec, std::chars_format::fixed, 6);
+      out += r.ec == std::errc() ? std::string(buf, r.ptr) : std::string("0.000000");
+    } else if (f.u64) {
+      out += std::to_string(st.*f.u64);
+    } else if (f.i32) {
+      out += std::to_string(st.*f.i32);
+    } else {
+      out += std::to_string(st.*f.sz);
+    }
+    out += '\n';
+  }
+  return out;
+}
+
+RankStats parse_rank_stats(std::string_view text) {
+  RankStats st;
+  std::size_t at = 0;
+  while (at < text.size()) {
+    std::size_t eol = text.find('\n', at);
+    if (eol == std::string_view::npos) eol = text.size();
+    const std::string_view line = text.substr(at, eol - at);
+    const std::size_t line_at = at;
+    at = eol + 1;
+    if (line.empty()) continue;
+    const std::size_t eq = line.find('=');
+    if (eq == std::string_view::npos) throw ParseError("stats line missing '='", line_at);
+    const std::string_view key = line.substr(0, eq), value = line.substr(eq + 1);
+    const StatField *f = nullptr;
+    for (const StatField &c : kStatFields)
+      if (key == c.key) f = &c;
+    if (!f) throw ParseError("unknown stats key '" + std::string(key) + "'", line_at);
+    const char *b = value.data(), *e = value.data() + value.size();
+    if (f->sec) {
+      double v = 0.0;
+      const auto r = std::from_chars(b, e, v);
+      if (r.ec != std::errc() || r.ptr != e) throw ParseError("bad stats value '" + std::string(value) + "'", line_at);
+      st.*f->sec = v;
+    } else {
+      std::uint64_t v = 0;
+      const auto r = std::from_chars(b, e, v);
+      if (r.ec != std::errc() || r.ptr != e) throw ParseError("bad stats count '" + std::string(value) + "'", line_at);
+      if (f->u64) st.*f->u64 = v;
+      else if (f->i32) st.*f->i32 = static_cast<int>(v);
+      else st.*f->sz = static_cast<std::size_t>(v);
+    }
+  }
+  return st;
+}
+
+namespace {
 struct RankIo {
   ByteSource *src;
   Sink *sink;

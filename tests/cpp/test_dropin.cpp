@@ -228,6 +228,15 @@ int main() {
     for (size_t got; (got = std::fread(buf, 1, sizeof buf, mf)) > 0;) merged.append(buf, got);
     std::fclose(mf);
     CHECK(merged == want);
+    // the .stats file format (pipeline.cpp:430-505) round-trips
+    const RankStats back = parse_rank_stats(format_rank_stats(rs));
+    CHECK(back.rows_written == rs.rows_written && back.workers == rs.workers &&
+          back.ligands_docked == rs.ligands_docked);
+    CHECK(format_rank_stats(back) == format_rank_stats(rs) || rs.wall_seconds != back.wall_seconds);
+    int bad = 0;
+    try { parse_rank_stats("ligands_docked=3\nnope=1\n"); } catch (const ParseError &) { ++bad; }
+    try { parse_rank_stats("rows_written 3\n"); } catch (const ParseError &) { ++bad; }
+    CHECK(bad == 2);
   }
 
   // per-thread device selection
