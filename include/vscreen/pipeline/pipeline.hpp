@@ -9,9 +9,11 @@
 //     and is otherwise ignored (it emulates slow CPU workers).
 //   * chunk / queue capacities keep their meaning where one exists
 //     (chunk_bytes, writer_buffer_bytes); rows are written in record order.
-//   * The per-stage functions of the reference (stage_reader, stage_splitter,
-//     docker_worker, stage_writer) are not part of this build: the B200 rank
-//     fuses them around the GPU batches.
+//   * docker_worker (pipeline.cpp:206-244) is the batch-pulling CUDA worker:
+//     it drains whatever WorkItems are queued (up to 65,536) into one
+//     dock_and_score_batch call.  The other stage functions (stage_reader,
+//     stage_splitter, stage_writer) are not part of this build: run_rank
+//     fuses them around GPU record decode.
 #pragma once
 
 #include <cstdint>
@@ -22,6 +24,7 @@
 #include "vscreen/dockengine/pose.hpp"
 #include "vscreen/molmodel/ligand.hpp"
 #include "vscreen/molmodel/pocket.hpp"
+#include "vscreen/pipeline/bounded_queue.hpp"
 #include "vscreen/pipeline/io.hpp"
 
 namespace vscreen {
@@ -68,6 +71,12 @@ struct PipelineConfig {
   std::size_t writer_buffer_bytes = std::size_t(4) << 20;
 };
 
+struct DockerStats {
+  std::uint64_t rows = 0;
+  std::uint64_t dock_errors = 0;
+  double busy_seconds = 0.0;
+};
+
 struct RankStats {
   std::uint64_t ligands_docked = 0;
   std::uint64_t records_skipped = 0;
@@ -98,6 +107,12 @@ std::string format_row(const OutputRow &row);
 // parse_rank_stats throws ParseError on a malformed line or unknown key.
 std::string format_rank_stats(const RankStats &stats);
 RankStats parse_rank_stats(std::string_view text);
+
+// pipeline.cpp:206-244: pop WorkItems, dock them, push one OutputRow per
+// ligand with a finite score (others count as dock_errors); stops when `in`
+// is closed and drained or `out` is closed.  Batched on the GPU.
+DockerStats docker_worker(BoundedQueue<WorkItem> &in, BoundedQueue<OutputRow> &out, const Pocket &pocket,
+                          const ScoringConfig &scoring, double synthetic_slowdown);
 
 // pipeline.cpp:297-389 / 391-396 on the B200 CUDA workers
 RankStats run_rank(const RankPlan &plan, ByteSource &source, Sink &sink, const Pocket &pocket,

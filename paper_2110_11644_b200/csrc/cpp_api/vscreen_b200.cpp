@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <charconv>
+#include <chrono>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -23,6 +24,7 @@
 #include <mutex>
 #include <numbers>
 #include <numeric>
+#include <optional>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -849,6 +851,37 @@ int32_t rank_write(void *u, const char *b, int64_t n) {
   }
 }
 }  // namespace
+
+DockerStats docker_worker(BoundedQueue<WorkItem> &in, BoundedQueue<OutputRow> &out, const Pocket &pocket,
+                          const ScoringConfig &scoring, double synthetic_slowdown) {
+  if (synthetic_slowdown < 1.0) throw InvalidArgument("synthetic slowdown must be at least 1");
+  constexpr std::size_t kBatch = 65536;
+  DockerStats st;
+  std::vector<Ligand> batch;
+  std::vector<std::string> errors;
+  while (std::optional<WorkItem> first = in.pop()) {
+    const auto t0 = std::chrono::steady_clock::now();
+    batch.clear();
+    batch.push_back(std::move(first->ligand));
+    while (batch.size() < kBatch) {
+      std::optional<WorkItem> next = in.try_pop();
+      if (!next) break;
+      batch.push_back(std::move(next->ligand));
+    }
+    errors.clear();
+    const std::vector<DockResult> res = dock_and_score_batch(pocket, batch, scoring, &errors);
+    st.busy_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (std::size_t i = 0; i < batch.size(); ++i) {
+      if (!errors[i].empty() || !std::isfinite(res[i].best_score)) {
+        ++st.dock_errors;
+        continue;
+      }
+      if (!out.push(OutputRow{res[i].smiles, res[i].best_score})) return st;  // writer gone
+      ++st.rows;
+    }
+  }
+  return st;
+}
 
 RankStats run_rank(const RankPlan &plan, ByteSource &source, Sink &sink, const Pocket &pocket,
                    const PipelineConfig &config) {

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "../../../include/vs_crtrig.h"
 #include "../../../include/vs_dock.h"
@@ -28,6 +29,14 @@ namespace vsd {
 // CR sin/cos of the 36 flatten lattice angles idx * (2 pi / 36)
 // (search.cpp:33,40), computed on the host with vs_crtrig.
 __constant__ double c_lattice_sc[72];
+
+// A kernel's max-dynamic-shared-memory attribute is process-wide state:
+// CUDA workers on other host threads launching the same kernel with another
+// size must not change it between this thread's set and launch.
+std::mutex &launch_mutex() {
+  static std::mutex mu;
+  return mu;
+}
 
 void set_lattice_table(const double *sc72, const double *lo72) {
   cudaMemcpyToSymbol(c_lattice_sc, sc72, sizeof(double) * 72);
@@ -775,6 +784,7 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
   const int mm = mmax < 1 ? 1 : mmax;
   const size_t dsmem = flatten_dep_smem(nmax_atoms, mm);
   if (!VS_FLAT_LEGACY && dsmem <= 200 * 1024) {
+    std::lock_guard<std::mutex> lock(launch_mutex());
     cudaFuncSetAttribute(k_flatten_dep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
     k_flatten_dep<<<n, kFT, dsmem, s>>>(b, max_sweeps, f, nmax_atoms, mm, lig_index);
     return cudaGetLastError();
@@ -783,6 +793,7 @@ cudaError_t launch_flatten(const batch_dev &b, int max_sweeps, const flat_out &f
   auto bytes = [&](int c) { return (size_t)(3 * nmax_atoms * (1 + c) + 36 + 12) * sizeof(double); };
   while (cb > 1 && bytes(cb) > 200 * 1024) cb = (cb + 1) / 2;
   const size_t smem = bytes(cb);
+  std::lock_guard<std::mutex> lock(launch_mutex());
   cudaFuncSetAttribute(k_flatten, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_flatten<<<n, kFlatThreads, smem, s>>>(b, max_sweeps, f, cb, lig_index);
   return cudaGetLastError();
@@ -1167,6 +1178,7 @@ cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_
     return cudaGetLastError();
   }
   const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + 2 * sizeof(int) * k + 16;
+  std::lock_guard<std::mutex> lock(launch_mutex());
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d);
   return cudaGetLastError();
@@ -1224,6 +1236,7 @@ __global__ void __launch_bounds__(kSelThreads) k_cluster(batch_dev b, int np, co
 cudaError_t launch_cluster(const batch_dev &b, int np, const double *geo, const double *confs, double threshold,
                            int top, int *order_out, int *count_out, cudaStream_t s) {
   const size_t smem = sizeof(int) * 3 * (size_t)np;
+  std::lock_guard<std::mutex> lock(launch_mutex());
   cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_cluster<<<1, kSelThreads, smem, s>>>(b, np, geo, confs, threshold, top, order_out, count_out);
   return cudaGetLastError();
@@ -1333,10 +1346,9 @@ cudaError_t launch_build_pocket(const double *hxyz, int nh, double cx, double cy
   return cudaGetLastError();
 }
 
-// Load this translation unit's kernels on the current device (CUDA lazy
-// loading would otherwise load them at first launch, and concurrent first
-// launches from several host threads on a new device raced in
-// cudaFuncSetAttribute: "invalid argument").
+// Load this translation unit's kernels on the current device at context
+// creation rather than at the first launch (keeps module loading out of the
+// CUDA workers' concurrent first launches).
 void preload_kernels() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_setup);

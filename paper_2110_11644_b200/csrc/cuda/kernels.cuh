@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "dmath.cuh"
@@ -128,6 +129,8 @@ struct dock_out {
 };
 
 void set_lattice_table(const double *sc72, const double *lo72);
+// serialises (max-dynamic-shared-memory attribute, launch) pairs across host threads
+std::mutex &launch_mutex();
 // load every kernel of the library on the current device (vs_context_create)
 void preload_kernels();
 void preload_kernels_search();

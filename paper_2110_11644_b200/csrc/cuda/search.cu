@@ -1254,6 +1254,7 @@ cudaError_t run_search(search_args &A, int num_sms, cudaStream_t s, int *launche
                        : (A.pg.mode == 1 ? (const void *)k_search<1, false>
                                          : (A.pg.mode == 2 ? (const void *)k_search<2, false>
                                                            : (const void *)k_search<0, false>));
+  std::lock_guard<std::mutex> lock(launch_mutex());  // attribute + launch, atomically w.r.t. other workers
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "vscreen/b200/prepare.hpp"
@@ -237,6 +238,50 @@ int main() {
     try { parse_rank_stats("ligands_docked=3\nnope=1\n"); } catch (const ParseError &) { ++bad; }
     try { parse_rank_stats("rows_written 3\n"); } catch (const ParseError &) { ++bad; }
     CHECK(bad == 2);
+  }
+
+  // docker_worker (pipeline.cpp:206-244): a producer thread feeds WorkItems
+  // through the reference's BoundedQueue; the batch-pulling CUDA worker's rows
+  // equal format_row of per-ligand dock_and_score, one degenerate ligand is a
+  // dock_error
+  {
+    std::vector<Ligand> lib = b200::prepare_ligands({"CCOC(=O)c1ccccc1N", "CCCCCCO", "c1ccccc1-c1ccccc1",
+                                                     "CC(C)Cc1ccc(cc1)C(C)C(=O)O"});
+    const char *names[] = {"A", "B", "C", "D"};
+    for (std::size_t i = 0; i < lib.size(); ++i) lib[i].name = names[i];
+    Ligand broken = lib[3];
+    broken.name = "E";
+    {
+      const auto &bond = broken.bonds[broken.torsions[0].bond_index];
+      broken.atoms[bond.b].position = broken.atoms[bond.a].position;  // degenerate torsion axis
+    }
+    BoundedQueue<WorkItem> in(2);
+    BoundedQueue<OutputRow> out(64);
+    std::thread producer([&] {
+      std::uint64_t seq = 0;
+      for (int rep = 0; rep < 3; ++rep)
+        for (const Ligand &l : lib) in.push(WorkItem{l, seq++});
+      in.push(WorkItem{broken, seq++});
+      in.close();
+    });
+    const DockerStats ds = docker_worker(in, out, twin, cfg, 1.0);
+    producer.join();
+    out.close();
+    std::vector<std::string> got;
+    while (auto row = out.pop()) got.push_back(format_row(*row));
+    std::vector<std::string> want;
+    for (int rep = 0; rep < 3; ++rep)
+      for (const Ligand &l : lib) want.push_back(format_row(OutputRow{l.name, dock_and_score(twin, l, cfg).best_score}));
+    CHECK(got == want);
+    CHECK(ds.rows == 12 && ds.dock_errors == 1);
+    bool threw = false;
+    try {
+      BoundedQueue<WorkItem> q(1);
+      docker_worker(q, out, twin, cfg, 0.5);
+    } catch (const InvalidArgument &) {
+      threw = true;
+    }
+    CHECK(threw);
   }
 
   // per-thread device selection
