@@ -135,3 +135,18 @@ def test_gpu_rank_over_two_devices(gpu_ctx, setup):
     got, st = api.run_rank(data, pocket, cfg, devices=[0, 1], batch_records=6, workers_per_device=2)
     assert got == want and st["workers"] == 4
     assert st["rows_written"] == wc["rows_written"] and st["records_skipped"] == wc["records_skipped"]
+
+
+@pytest.mark.gpu
+def test_gpu_rank_k40_and_default_config(gpu_ctx, setup):
+    """k > 32 (the CTA select) and the reference's default ScoringConfig
+    (k=256, rescored=30) through the rank pipeline, against the reference's
+    own run_rank on the first 12 records."""
+    ref, pocket, data, _ = setup
+    spans = record_spans(data, 8)
+    small = data[:spans[12][0]]
+    for cfg in (abi.ScoringConfig(restarts=40, rescored=7), abi.ScoringConfig()):
+        want, wc = ref.run_rank(small, pocket, cfg)
+        got, st = api.run_rank(small, pocket, cfg, devices=[0], batch_records=5)
+        assert got == want
+        assert st["records_skipped"] == wc["records_skipped"] == 1
