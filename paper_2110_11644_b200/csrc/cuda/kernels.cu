@@ -348,6 +348,17 @@ __global__ void __launch_bounds__(kFlatThreads) k_flatten(batch_dev b, int max_s
 //     groups, ~2% of decisions) get the exact sequential sum of the legacy
 //     kernel, and the argmax is taken over those exact values.
 // The decision, and so every output, is bit-identical to the legacy kernel.
+#ifdef VS_FLAT_PROF  // development only: thread 0's clock64() time per phase (tools/flat_prof.py)
+__device__ unsigned long long g_fphase[16];  // 0-6 phases, 7 CTAs, 8 decisions, 9 exact near-tie paths
+#define FP_MARK(k)                             \
+  if (tid == 0) {                              \
+    const unsigned long long fp_n = clock64(); \
+    fp_acc[k] += fp_n - fp_t;                  \
+    fp_t = fp_n;                               \
+  }
+#else
+#define FP_MARK(k)
+#endif
 constexpr int kFC = 36;         // candidates per torsion (10-degree lattice offsets)
 constexpr int kFL = 8;          // lanes per candidate
 constexpr int kFT = kFC * kFL;  // 288 threads = 9 full warps
@@ -420,6 +431,9 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
     s_ver = 0;
   }
   __syncthreads();
+#ifdef VS_FLAT_PROF
+  unsigned long long fp_acc[8] = {0}, fp_t = clock64();
+#endif
   for (int sweep = 0; sweep < max_sweeps && m > 0; ++sweep) {
     if (sweep) __syncthreads();  // every thread has read the previous sweep's `changed`
     if (tid == 0) {
@@ -509,6 +523,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         }
       }
       __syncthreads();
+      FP_MARK(0)
       if (bad) break;
       const bool skipping = s_skip;
       if (!skipping) {
@@ -554,6 +569,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
             }
           __syncwarp();
         }
+        FP_MARK(1)
         // ---- C: filter sum over the pairs that touch D_t, in two flattened
         // walks strided by the 8 lanes of the candidate: (rank r, common k),
         // then (rank r, rank s > r).
@@ -630,7 +646,9 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           if (g == 0) spread[o] = acc;
         }
       }  // !skipping
+      FP_MARK(2)
       __syncthreads();  // (skipping: every thread has read bad and s_skip)
+      FP_MARK(3)
       // ---- D (warp 0): certain winner, or the exact sums of the candidates
       // within rounding of it; then the prefix advance (search.cpp:52-60)
       if (tid < 32) {
@@ -668,6 +686,13 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           w = 1ull << bo;
 #endif
           best_off = bo;
+          FP_MARK(4)
+#ifdef VS_FLAT_PROF
+          if (lane == 0) {
+            atomicAdd(&g_fphase[8], 1ull);
+            if (__popcll(w) > 1) atomicAdd(&g_fphase[9], 1ull);
+          }
+#endif
           if (__popcll(w) > 1) {
             // exact sequential sums (transform.cpp:83-90) of the near-tied
             // candidates, first argmax among them
@@ -719,6 +744,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
             }
             best_off = ev == ninf ? 0 : eo;
           }
+          FP_MARK(5)
         }  // !skipping
         const int nidx = (idx[t] + best_off) % 36;
         __syncwarp();
@@ -739,10 +765,17 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           if ((tms[a] >> t) & 1u) st3(P + 3 * a, torsion_apply(M, ld3(P + 3 * a)));
         __syncwarp();
       }
+      FP_MARK(6)
     }
     __syncthreads();
     if (bad || !changed) break;
   }
+#ifdef VS_FLAT_PROF
+  if (tid == 0) {
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_fphase[k], fp_acc[k]);
+    atomicAdd(&g_fphase[7], 1ull);
+  }
+#endif
   if (bad) {
     if (tid == 0) b.meta[l].status = VS_LIG_DEGENERATE_AXIS;
     return;
@@ -772,6 +805,17 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   if (tid < 3) f.centroid[3 * l + tid] = centroid_row(P, N, tid);
   if (tid == 0) f.sweeps[l] = sweeps_done;
 }
+
+#ifdef VS_FLAT_PROF
+extern "C" int vs_debug_flat_phase_read(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_fphase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_fphase, z, sizeof z);
+  }
+  return 0;
+}
+#endif
 
 #ifndef VS_FLAT_LEGACY
 #define VS_FLAT_LEGACY 0  // A/B only: 1 = always the legacy kernel
