@@ -283,6 +283,52 @@ __device__ __noinline__ int chain_warp(int vbase, int ufrom, int m, const double
   return bad;
 }
 
+// The same chains with two lanes per variant, one per axis endpoint
+// (lane = 2 (v - vbase) + e, 16 variants per call): every carried transform
+// is one 3-vector per lane instead of two, halving the chain's FP64
+// instructions; the pair exchanges its endpoints by shuffles before the
+// Rodrigues build, which both lanes evaluate and store (identical bits).
+#ifndef VS_CHAIN_SPLIT
+#define VS_CHAIN_SPLIT 1
+#endif
+__device__ __noinline__ int chain_warp2(int vbase32, int ufrom, int m, const double *ep, const uint32_t *epm,
+                                        const double *Mcur, const double *sccur, const double *cache, double *Mvar,
+                                        int lane) {
+  int bad = 0;
+  const int e = lane & 1;
+  #pragma unroll 1
+  for (int vbase = vbase32; vbase < 2 * m && vbase < vbase32 + 32; vbase += 16) {
+    const int v = vbase + (lane >> 1);
+    const bool act = v < 2 * m;
+    const int t = act ? (v >> 1) : m;
+    double *out = Mvar + (act ? mvar_off(v, t, m) : 0);
+    #pragma unroll 1
+    for (int u = max(vbase >> 1, ufrom); u < m; ++u) {
+      d3 x = ld3(ep + 6 * u + 3 * e);
+      const uint32_t mk = epm[2 * u + e], mab = epm[2 * u] | epm[2 * u + 1];
+      #pragma unroll 1
+      for (uint32_t bb = mab & ((1u << u) - 1u); bb; bb &= bb - 1u) {
+        const int w = __ffs(bb) - 1;
+        const double *M = w < t ? Mcur + 12 * w : out + 12 * (w - t);
+        double r[12];
+        ld12a(M, r);
+        const d3 nx = torsion_apply(r, x);
+        if ((mk >> w) & 1u) x = nx;
+      }
+      const d3 y{__shfl_xor_sync(0xffffffffu, x.x, 1), __shfl_xor_sync(0xffffffffu, x.y, 1),
+                 __shfl_xor_sync(0xffffffffu, x.z, 1)};
+      if (u >= t) {
+        const double s = u == t ? cache[2 * v] : sccur[2 * u];
+        const double c = u == t ? cache[2 * v + 1] : sccur[2 * u + 1];
+        // both lanes of the pair store the same bits
+        if (!torsion_setup(e ? y : x, e ? x : y, s, c, out + 12 * (u - t))) bad = 1;
+      }
+      __syncwarp();  // the pair's new matrix is visible to both lanes
+    }
+  }
+  return bad;
+}
+
 // Torsioned frame (search.cpp:115) of the hydrogens into the warp's global
 // scratch `hx` (atom order; apply_torsions per atom, transform.cpp:73-81).
 // The search keeps only heavy atoms in shared memory: hydrogens matter only
@@ -829,7 +875,11 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
           pr_sc += (unsigned int)(clock64() - pr0);
           pr0 = clock64();
 #endif
+#if VS_CHAIN_SPLIT
+          if (chain_warp2(vb0, chain_from, m, s_ep, s_epm, Mcur, sccur, cache, Mvar, lane)) S[S_ERR] = 1.0;
+#else
           if (chain_warp(vb0, chain_from, m, s_ep, s_epm, Mcur, sccur, cache, Mvar, lane)) S[S_ERR] = 1.0;
+#endif
 #ifdef VS_PHASE_PROF
           __syncwarp();
           pr_ch += (unsigned int)(clock64() - pr0);
