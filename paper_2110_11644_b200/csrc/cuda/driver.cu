@@ -85,7 +85,7 @@ struct vs_context {
   // flatten / search / select
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
-  DevBuf results, best_ang, best_conf, counters, spin, fibq, stepsc, flat_index;
+  DevBuf results, best_ang, best_conf, best_idx, counters, spin, fibq, stepsc, flat_index;
   DevBuf aux0, aux1, aux2, aux3, search_args, lig_index;
   // record decode
   DevBuf dec_bytes, dec_offs, dec_aoff, dec_boff, dec_toff, dec_rsoff, dec_xyz, dec_elem, dec_heavy, dec_order,
@@ -936,9 +936,11 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
     vsd::item_out o{};
     if ((rc = ensure_flat(ctx, st, f))) return rc;
     if ((rc = ensure_items(ctx, st, k, o))) return rc;
+    o.heavy_conf = 1;
     CUDA_TRY(ctx->results.ensure(sizeof(vs_dock_result) * std::max(st.n, 1)));
     CUDA_TRY(ctx->best_ang.ensure(sizeof(double) * std::max(st.torsions, 1)));
     CUDA_TRY(ctx->best_conf.ensure(sizeof(double) * 3 * std::max(st.atoms, 1)));
+    CUDA_TRY(ctx->best_idx.ensure(sizeof(int) * std::max(st.n, 1)));
     CUDA_TRY(ctx->counters.ensure(sizeof(uint64_t) * 9 * std::max(st.n, 1)));
     CUDA_TRY(cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[0], ctx->stream));
@@ -961,7 +963,8 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
     double *best_conformation = best_conf_p ? best_conf_p[pi] : nullptr;
     uint64_t *counters = counters_p ? counters_p[pi] : nullptr;
     vsd::dock_out d{ctx->results.p, ctx->best_ang.as<double>(), ctx->best_conf.as<double>(),
-                    counters ? ctx->counters.as<unsigned long long>() : nullptr, f.sweeps};
+                    counters ? ctx->counters.as<unsigned long long>() : nullptr, f.sweeps,
+                    ctx->best_idx.as<int>()};
     if (pi > 0) CUDA_TRY(cudaEventRecord(ctx->evs[2], ctx->stream));
     {
       // Size buckets: ligands grouped by how many 4-warp search CTAs per SM
@@ -1011,7 +1014,7 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
     CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
     CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));
-    ctx->last_launches += pi == 0 ? 4 : 2;
+    ctx->last_launches += (pi == 0 ? 4 : 2) + 1;  // + k_best_conf (d.best_conf is always set)
     CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,
                              ctx->stream));
     const int T0 = batch ? batch->torsion_offset[l0] : 0, A0 = batch ? batch->atom_offset[l0] : 0;

@@ -886,16 +886,56 @@ __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, dou
   }
 }
 
+// chem_score of a compact heavy-atom conformation (heavy atom h at 3h).
 __device__ double chem_pose(const pocket_dev &p, const double *conf, const uint16_t *hl, const uint8_t *elem, int n,
                             int &clashes, int &pairs) {
   double total = 0.0;
   clashes = 0;
   pairs = 0;
-  for (int h = 0; h < n; ++h) {
-    const int a = hl[h];
-    chem_atom(p, ld3(conf + 3 * a), chem_class_of(elem[a]), total, clashes, pairs);
-  }
+  for (int h = 0; h < n; ++h) chem_atom(p, ld3(conf + 3 * h), chem_class_of(elem[hl[h]]), total, clashes, pairs);
   return total;
+}
+
+// The best pose's full conformation (atom order) from its compact heavy-atom
+// conformation, its angles and its transform: heavy atoms copied (the bits
+// k_search produced), hydrogens rematerialised as apply_rigid(
+// apply_torsions(base, angles), T) (pose.hpp:20-22; transform.cpp:73-81,
+// 31): lane 0 rebuilds the torsion matrices from the base coordinates and
+// the correctly rounded sin/cos of the final angles -- the values and
+// operations of k_search's chains -- then the lanes carry the hydrogens.
+// M: 12 m doubles of scratch.  Warp-cooperative.
+__device__ void best_conformation(const batch_dev &b, int l, const double *hc, const double *ang, const double *T7,
+                                  double *M, double *out, int lane) {
+  const lig_meta meta = b.meta[l];
+  const int N = meta.n_atoms, n = meta.n_heavy, m = meta.m;
+  const int a0 = b.atom_off[l], t0 = b.tors_off[l];
+  const double *base = b.xyz + 3 * (size_t)a0;
+  const uint32_t *tm = b.atom_tmask + a0;
+  const uint16_t *hl = b.heavy_list + a0;
+  if (lane == 0)
+    for (int t = 0; t < m; ++t) {
+      const int ia = b.tors_a[t0 + t], ib = b.tors_b[t0 + t];
+      d3 pa = ld3(base + 3 * ia), pb = ld3(base + 3 * ib);
+      const uint32_t ma = tm[ia], mb = tm[ib];
+      for (int w = 0; w < t; ++w) {
+        if ((ma >> w) & 1u) pa = torsion_apply(M + 12 * w, pa);
+        if ((mb >> w) & 1u) pb = torsion_apply(M + 12 * w, pb);
+      }
+      double sn, cs;
+      vs_crtrig::sincos_cr(ang[t], &sn, &cs);
+      torsion_setup(pa, pb, sn, cs, M + 12 * t);  // k_search built this axis: not degenerate
+    }
+  __syncwarp();
+  double R[9];
+  quat_matrix(quat{T7[0], T7[1], T7[2], T7[3]}, R);
+  const double tr[3] = {T7[4], T7[5], T7[6]};
+  for (int h = lane; h < n; h += 32) st3(out + 3 * (size_t)hl[h], ld3(hc + 3 * h));
+  for (int a = lane; a < N; a += 32) {
+    if (b.heavy[a0 + a]) continue;
+    d3 x = ld3(base + 3 * a);
+    for (uint32_t bb = tm[a]; bb; bb &= bb - 1u) x = torsion_apply(M + 12 * (__ffs(bb) - 1), x);
+    st3(out + 3 * (size_t)a, rigid_col(R, tr, x, a));
+  }
 }
 
 __device__ __forceinline__ int f_sweeps_of(const dock_out &d, int l) { return d.sweeps ? d.sweeps[l] : 0; }
@@ -935,6 +975,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
       vs_dock_result z{};
       z.status = status;
       *res = z;
+      if (d.best_idx) d.best_idx[l] = -1;
     }
     return;
   }
@@ -942,7 +983,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   const int a0 = b.atom_off[l], t0 = b.tors_off[l];
   const uint16_t *hl = b.heavy_list + a0;
   const double *geo = o.geo + (size_t)l * k;
-  const double *confs = o.conf + 3 * (size_t)a0 * k;  // pose r at + 3*r*N
+  const double *confs = o.conf + 3 * (size_t)a0 * k;  // pose r at + 3*r*N, heavy atoms compact
   // stable sort by descending geo_score (search.cpp:201-206)
   for (int i = tid; i < k; i += blockDim.x) {
     const double gi = geo[i];
@@ -964,10 +1005,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
     for (int li = tid; li < nl; li += blockDim.x) {
       const double *cl = confs + 3 * (size_t)leaders[li] * N;
       double sum = 0.0;
-      for (int h = 0; h < n; ++h) {
-        const int a = hl[h];
-        sum += sqn3(sub3(ld3(ci + 3 * a), ld3(cl + 3 * a)));
-      }
+      for (int h = 0; h < n; ++h) sum += sqn3(sub3(ld3(ci + 3 * h), ld3(cl + 3 * h)));
       if (dsqrt(sum / (double)n) <= c.rmsd_threshold) atomicMin(&first_match, li);
     }
     __syncthreads();
@@ -1006,8 +1044,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   const int bs = best_s;
   const int bidx = bs < n_lead ? leaders[bs] : followers[bs - n_lead];
   const double *bconf = confs + 3 * (size_t)bidx * N;
-  if (d.best_conf)
-    for (int i = tid; i < 3 * N; i += blockDim.x) d.best_conf[3 * (size_t)a0 + i] = bconf[i];
+  if (tid == 0 && d.best_idx) d.best_idx[l] = bidx;
   if (d.best_ang)
     for (int u = tid; u < m; u += blockDim.x) d.best_ang[t0 + u] = o.ang[(size_t)t0 * k + (size_t)bidx * m + u];
   __shared__ int oob;
@@ -1015,7 +1052,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
   __syncthreads();
   for (int h = tid; h < n; h += blockDim.x) {
     bool out;
-    field_value(p.g, ld3(bconf + 3 * hl[h]), out);
+    field_value(p.g, ld3(bconf + 3 * h), out);
     if (out) atomicAdd(&oob, 1);
   }
   __syncthreads();
@@ -1088,6 +1125,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_select_warp(batch_dev b, poc
       vs_dock_result z{};
       z.status = status;
       *res = z;
+      if (d.best_idx) d.best_idx[l] = -1;
     }
     return;
   }
@@ -1095,7 +1133,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_select_warp(batch_dev b, poc
   const int a0 = b.atom_off[l], t0 = b.tors_off[l];
   const uint16_t *hl = b.heavy_list + a0;
   const double *geo = o.geo + (size_t)l * k;
-  const double *confs = o.conf + 3 * (size_t)a0 * k;  // pose r at + 3*r*N
+  const double *confs = o.conf + 3 * (size_t)a0 * k;  // pose r at + 3*r*N, heavy atoms compact
   // stable sort by descending geo_score (search.cpp:201-206)
   if (lane < k) {
     const double gi = geo[lane];
@@ -1121,10 +1159,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_select_warp(batch_dev b, poc
       // unrolled: the L2 loads of several atoms are in flight ahead of the
       // sequential sum (whose order is unchanged)
       #pragma unroll kSelUnroll
-      for (int h = 0; h < n; ++h) {
-        const int a = hl[h];
-        sum += sqn3(sub3(ld3(ci + 3 * a), ld3(cl + 3 * a)));
-      }
+      for (int h = 0; h < n; ++h) sum += sqn3(sub3(ld3(ci + 3 * h), ld3(cl + 3 * h)));
       match = dsqrt(sum / (double)n) <= c.rmsd_threshold;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, match);
@@ -1167,14 +1202,13 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_select_warp(batch_dev b, poc
   for (int off = 16; off > 0; off >>= 1) pchem += __shfl_xor_sync(0xffffffffu, pchem, off);
   const int bidx = bs < n_lead ? leaders[bs] : followers[bs - n_lead];
   const double *bconf = confs + 3 * (size_t)bidx * N;
-  if (d.best_conf)
-    for (int i = lane; i < 3 * N; i += 32) d.best_conf[3 * (size_t)a0 + i] = bconf[i];
+  if (lane == 0 && d.best_idx) d.best_idx[l] = bidx;
   if (d.best_ang)
     for (int u = lane; u < m; u += 32) d.best_ang[t0 + u] = o.ang[(size_t)t0 * k + (size_t)bidx * m + u];
   int oob = 0;
   for (int h = lane; h < n; h += 32) {
     bool out;
-    field_value(p.g, ld3(bconf + 3 * hl[h]), out);
+    field_value(p.g, ld3(bconf + 3 * h), out);
     oob += out ? 1 : 0;
   }
   oob = __reduce_add_sync(0xffffffffu, oob);
@@ -1218,19 +1252,40 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_select_warp(batch_dev b, poc
   }
 }
 
+// The best pose's full conformation (best_conformation), one warp per ligand,
+// after the select (its own kernel: the rematerialisation's registers would
+// halve the select's occupancy).
+__global__ void __launch_bounds__(32 * kSelWarps) k_best_conf(batch_dev b, search_cfg c, item_out o, dock_out d) {
+  __shared__ double s_M[kSelWarps][12 * VS_MAX_TORSIONS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int l = blockIdx.x * kSelWarps + w;
+  if (l >= b.n_lig) return;
+  const int bidx = d.best_idx[l];
+  if (bidx < 0) return;
+  const int k = c.k, m = b.meta[l].m;
+  const int a0 = b.atom_off[l], t0 = b.tors_off[l];
+  const size_t item = (size_t)l * k + bidx;
+  best_conformation(b, l, o.conf + 3 * ((size_t)a0 * k + (size_t)bidx * b.meta[l].n_atoms),
+                    o.ang + (size_t)t0 * k + (size_t)bidx * m, o.T + 7 * item, s_M[w], d.best_conf + 3 * (size_t)a0,
+                    lane);
+}
+
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
                           const dock_out &d, int nmax_atoms, cudaStream_t s) {
   (void)nmax_atoms;
   if (b.n_lig == 0) return cudaSuccess;
+  if (!o.heavy_conf) return cudaErrorInvalidValue;  // the selects read compact heavy-atom conformations
   const int k = c.k;
+  if (d.best_conf && !d.best_idx) return cudaErrorInvalidValue;
   if (k <= 32) {
     k_select_warp<<<(b.n_lig + kSelWarps - 1) / kSelWarps, 32 * kSelWarps, 0, s>>>(b, p, c, o, d);
-    return cudaGetLastError();
+  } else {
+    const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + 2 * sizeof(int) * k + 16;
+    std::lock_guard<std::mutex> lock(launch_mutex());
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d);
   }
-  const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + 2 * sizeof(int) * k + 16;
-  std::lock_guard<std::mutex> lock(launch_mutex());
-  cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d);
+  if (d.best_conf) k_best_conf<<<(b.n_lig + kSelWarps - 1) / kSelWarps, 32 * kSelWarps, 0, s>>>(b, c, o, d);
   return cudaGetLastError();
 }
 

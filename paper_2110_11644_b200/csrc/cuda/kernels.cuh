@@ -106,7 +106,9 @@ struct item_out {
   double *geo;              // items
   double *T;                // items * 7 (q xyzw, t xyz)
   double *ang;              // tors_off[l]*k + r*m + t
-  double *conf;             // (atom_off[l]*k + r*N + a)*3
+  double *conf;             // (atom_off[l]*k + r*N + a)*3; heavy_conf: heavy atom h at + 3*h
+  int heavy_conf;           // dock path: restart conformations hold the heavy atoms only (select reads
+                            // nothing else; the best pose's hydrogens are rematerialised)
   unsigned long long *evals;
   int *status;
   int *iters;               // items: local_search iterations
@@ -126,6 +128,7 @@ struct dock_out {
   double *best_conf;        // 3*atoms
   unsigned long long *counters;  // n*9 (may be NULL): S, A_rigid, A_tors, R_build, P_flat, P_chem, P_rmsd, clash, oob
   const int *sweeps;        // flatten sweeps per ligand (flat_out.sweeps)
+  int *best_idx;            // n: restart of the best pose, -1 without a result (k_best_conf input)
 };
 
 void set_lattice_table(const double *sc72, const double *lo72);

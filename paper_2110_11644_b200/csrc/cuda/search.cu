@@ -454,12 +454,17 @@ __device__ __forceinline__ void screen_map(const float *S, float x0, float x1, f
 // The whole conformation of the current pose into `out` (3N, atom order):
 // the torsioned frame `hx` (global scratch, every atom), then apply_rigid
 // (transform.cpp:31) when `rigid`.
+// hl != NULL (dock path outputs): only the heavy atoms, compact (heavy atom h
+// at 3h, atom hl[h]) -- all that cluster_and_select and chem_score read; the
+// best pose's hydrogens are rematerialised by the select (kernels.cu
+// best_conformation).
 __device__ __noinline__ void full_conformation(double *out, const double *S, int N, const double *hx, bool rigid,
-                                               int lane) {
+                                               int lane, const uint32_t *hl = nullptr) {
   #pragma unroll 1
-  for (int a = lane; a < N; a += 32) {
+  for (int i = lane; i < N; i += 32) {
+    const int a = hl ? (int)hl[i] : i;
     const d3 x = ld3(hx + 3 * a);
-    st3(out + 3 * a, rigid ? rigid_col_rt(S + S_R, S + S_T, x, a) : x);
+    st3(out + 3 * i, rigid ? rigid_col_rt(S + S_R, S + S_T, x, a) : x);
   }
 }
 
@@ -1206,7 +1211,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
       #pragma unroll 1
       for (int i = lane; i < 3 * N; i += 32) A.o.conf[ck + i] = A.conf_in[3 * (size_t)a0 + i];
     } else {
-      full_conformation(A.o.conf + ck, S, N, hx, true, lane);
+      full_conformation(A.o.conf + ck, S, A.o.heavy_conf ? n : N, hx, true, lane, A.o.heavy_conf ? s_hl : nullptr);
     }
     const size_t tk = (size_t)t0 * k + (size_t)r * m;
     #pragma unroll 1
