@@ -1168,8 +1168,11 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
             }
             st3(hx + 3 * s_hl[h], x);
           }
+          PH(19)
           hydrogen_frame(hx, N, base, tm, hv, Mcur, dep, lane);
+          PH(20)
           prefix_frame(pc, s_tit, s_doff[t] + s_dcnt[t], meta.d_total, s_bh, s_tmh, Mcur, lane);
+          PH(21)
           if (SCR) {
             __syncwarp();
             Xf = frame_max32(t32, n, lane);
