@@ -288,6 +288,13 @@ __device__ __noinline__ int chain_warp(int vbase, int ufrom, int m, const double
 // is one 3-vector per lane instead of two, halving the chain's FP64
 // instructions; the pair exchanges its endpoints by shuffles before the
 // Rodrigues build, which both lanes evaluate and store (identical bits).
+#ifndef VS_ROW_UNROLL
+#define VS_ROW_UNROLL 2  // neighbour row sums: loads in flight ahead of the sequential adds (measured with
+                         // VS_CENTROID_UNROLL 2: 1 -> 724 ms, 2 -> 696 ms, 4 -> 702 ms, 8 -> 726 ms search per step;
+                         // code-layout sensitive: the hot loop sits at the 32 KB instruction-cache limit)
+#endif
+constexpr int kRowUnroll = VS_ROW_UNROLL;
+
 #ifndef VS_CHAIN_SPLIT
 #define VS_CHAIN_SPLIT 1
 #endif
@@ -1075,12 +1082,12 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
             // heavy atoms outside D_t sample exactly as in the current pose:
             // their values come from vcur (the row holds only D_t's samples)
             const uint32_t tb = 1u << (tlo + (lane >> 1));
-            #pragma unroll 4
+            #pragma unroll kRowUnroll
             for (int h = 0; h < n; ++h) acc += (s_dm[h] & tb) ? row[h] : vcur[h];
           } else
 #endif
           {
-            #pragma unroll 4
+            #pragma unroll kRowUnroll
             for (int h = 0; h < n; ++h) acc += row[h];
           }
           gacc = acc;
