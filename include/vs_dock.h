@@ -64,7 +64,7 @@ typedef enum vs_ligand_status {
 #define VS_MAX_ATOMS 256
 #define VS_MAX_HEAVY 128
 #define VS_MAX_TORSIONS 31
-#define VS_MAX_RESTARTS 1024
+#define VS_MAX_RESTARTS 65536 /* k <= ~7000: select state in shared memory, beyond in global */
 
 /* Element codes: wire-stable, elements.hpp:14-26. */
 enum {

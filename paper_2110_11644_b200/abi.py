@@ -42,7 +42,7 @@ LIGAND_STATUS_NAMES = {
 VS_MAX_ATOMS = 256
 VS_MAX_HEAVY = 128
 VS_MAX_TORSIONS = 31
-VS_MAX_RESTARTS = 1024
+VS_MAX_RESTARTS = 65536
 
 _d = C.POINTER(C.c_double)
 _i32 = C.POINTER(C.c_int32)

@@ -85,7 +85,7 @@ struct vs_context {
   // flatten / search / select
   DevBuf flat_idx, flat_xyz, flat_centroid, flat_sweeps, out_geo, out_T, out_ang, out_conf, out_evals, out_status,
       out_iters, out_adopts, work;
-  DevBuf results, best_ang, best_conf, best_idx, counters, spin, fibq, stepsc, flat_index;
+  DevBuf results, best_ang, best_conf, best_idx, sel_scratch, counters, spin, fibq, stepsc, flat_index;
   DevBuf aux0, aux1, aux2, aux3, search_args, lig_index;
   // record decode
   DevBuf dec_bytes, dec_offs, dec_aoff, dec_boff, dec_toff, dec_rsoff, dec_xyz, dec_elem, dec_heavy, dec_order,
@@ -1012,7 +1012,8 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
       --ctx->last_launches;  // counted once below with the fixed launches
     }
     CUDA_TRY(cudaEventRecord(ctx->evs[3], ctx->stream));
-    CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream));
+    if (const size_t sb = vsd::select_scratch_bytes(st.n, k)) CUDA_TRY(ctx->sel_scratch.ensure(sb));
+    CUDA_TRY(vsd::launch_select(st.b, pd, sc, o, d, st.Nmax, ctx->stream, ctx->sel_scratch.as<int>()));
     CUDA_TRY(cudaEventRecord(ctx->evs[4], ctx->stream));
     ctx->last_launches += (pi == 0 ? 4 : 2) + 1;  // + k_best_conf (d.best_conf is always set)
     CUDA_TRY(cudaMemcpyAsync(results + l0, ctx->results.p, sizeof(vs_dock_result) * st.n, cudaMemcpyDeviceToHost,

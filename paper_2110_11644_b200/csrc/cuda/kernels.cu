@@ -945,10 +945,18 @@ __device__ __forceinline__ int f_sweeps_of(const dock_out &d, int l) { return d.
 // ligand.
 constexpr int kSelThreads = 128;
 
-__global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev p, search_cfg c, item_out o, dock_out d) {
-  extern __shared__ int si[];
+// Per-ligand select state (ints): order, leaders, followers (3k), chem
+// (k doubles, 8-byte aligned), clash, pairs (2k).
+__host__ __device__ inline size_t select_state_ints(int k) { return (size_t)3 * k + (k & 1) + 2 + 2 * (size_t)k + 2 * k + 4; }
+
+__global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev p, search_cfg c, item_out o, dock_out d,
+                                                        int *gs) {
+  extern __shared__ int sdyn[];
   const int l = blockIdx.x, tid = threadIdx.x;
   const int k = c.k;
+  // shared memory, or a per-ligand slice of global scratch for restart
+  // counts whose state exceeds it
+  int *si = gs ? gs + select_state_ints(k) * (size_t)l : sdyn;
   int *order = si;            // k
   int *leaders = order + k;   // k
   int *followers = leaders + k;
@@ -1270,8 +1278,16 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_best_conf(batch_dev b, searc
                     lane);
 }
 
+constexpr size_t kSelSmemMax = 160 * 1024;
+
+size_t select_scratch_bytes(int n_lig, int k) {
+  return k > 32 && select_state_ints(k) * sizeof(int) > kSelSmemMax
+             ? select_state_ints(k) * sizeof(int) * (size_t)(n_lig > 0 ? n_lig : 1)
+             : 0;
+}
+
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
-                          const dock_out &d, int nmax_atoms, cudaStream_t s) {
+                          const dock_out &d, int nmax_atoms, cudaStream_t s, int *sel_scratch) {
   (void)nmax_atoms;
   if (b.n_lig == 0) return cudaSuccess;
   if (!o.heavy_conf) return cudaErrorInvalidValue;  // the selects read compact heavy-atom conformations
@@ -1279,11 +1295,14 @@ cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_
   if (d.best_conf && !d.best_idx) return cudaErrorInvalidValue;
   if (k <= 32) {
     k_select_warp<<<(b.n_lig + kSelWarps - 1) / kSelWarps, 32 * kSelWarps, 0, s>>>(b, p, c, o, d);
-  } else {
-    const size_t smem = sizeof(int) * (3 * k + (k & 1) + 2) + sizeof(double) * k + 2 * sizeof(int) * k + 16;
+  } else if (select_state_ints(k) * sizeof(int) <= kSelSmemMax) {
+    const size_t smem = select_state_ints(k) * sizeof(int);
     std::lock_guard<std::mutex> lock(launch_mutex());
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d);
+    k_select<<<b.n_lig, kSelThreads, smem, s>>>(b, p, c, o, d, nullptr);
+  } else {
+    if (!sel_scratch) return cudaErrorInvalidValue;  // select_scratch_bytes of global scratch
+    k_select<<<b.n_lig, kSelThreads, 0, s>>>(b, p, c, o, d, sel_scratch);
   }
   if (d.best_conf) k_best_conf<<<(b.n_lig + kSelWarps - 1) / kSelWarps, 32 * kSelWarps, 0, s>>>(b, c, o, d);
   return cudaGetLastError();

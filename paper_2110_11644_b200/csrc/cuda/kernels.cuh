@@ -159,7 +159,10 @@ size_t search_scratch_bytes(int nmax_atoms, int nmax_heavy, int mmax, int num_sm
 size_t search_smem_bytes(int N, int n, int m, int dtot, bool screen);
 int search_warps_per_cta();
 cudaError_t launch_select(const batch_dev &b, const pocket_dev &p, const search_cfg &c, const item_out &o,
-                          const dock_out &d, int nmax_atoms, cudaStream_t s);
+                          const dock_out &d, int nmax_atoms, cudaStream_t s, int *sel_scratch = nullptr);
+// global scratch the select needs for restart counts whose per-ligand state
+// exceeds shared memory (0 otherwise)
+size_t select_scratch_bytes(int n_lig, int k);
 // sub-API kernels
 cudaError_t launch_field_values(const pocket_dev &p, int64_t n, const double *xyz, double *out, cudaStream_t s);
 cudaError_t launch_geo_score(const batch_dev &b, const pocket_dev &p, const double *conf, double *out,

@@ -319,6 +319,23 @@ def test_dock_default_config_256_restarts(env):
     assert np.array_equal(got.best_conformation, want["conformation"])
 
 
+@pytest.mark.parametrize("k", [2048, 8192])
+def test_dock_restart_counts_beyond_shared_memory(env, k):
+    """Restart counts far above the default: k = 2048 keeps the select state
+    in shared memory, k = 8192 moves it to global scratch; both bit-exact
+    against the oracle (search.cpp:238-276 accepts any restart count)."""
+    ctx, pocket, host, b = env
+    small = sorted(b.ligands, key=lambda l: (l.n_atoms, l.name))[:2]
+    sub = LigandBatch(small)
+    cfg = abi.ScoringConfig(restarts=k, rescored=30)
+    got = api.dock_and_score_batch(pocket, sub, cfg, ctx)
+    want = Oracle("port", trig=1).dock_batch(host, sub, cfg, nthreads=THREADS)
+    assert np.array_equal(got.results["status"], want["results"]["status"])
+    assert np.array_equal(got.results["best_score"], want["results"]["best_score"])
+    assert np.array_equal(got.results["scoring_evals"], want["results"]["scoring_evals"])
+    assert np.array_equal(got.best_conformation, want["conformation"])
+
+
 # ------------------------------------------------------------------ edge cases
 def _lig(name, xyz, elem, heavy, bonds=(), orders=None, tors=(), rights=()):
     bonds = np.array(bonds, dtype=np.uint16).reshape(-1, 2)
