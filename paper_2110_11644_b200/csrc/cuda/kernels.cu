@@ -375,8 +375,75 @@ __device__ __forceinline__ double dsqrt_filter(double x) {
 }
 
 size_t flatten_dep_smem(int nmax, int mmax) {
-  return (size_t)(3 * nmax + 3 * nmax + 4 * nmax + 3 * nmax * kFC + 18 * mmax + kFC) * sizeof(double) +
+  return (size_t)(3 * nmax + 3 * nmax + 4 * nmax + 3 * nmax * kFC + 18 * mmax + 3 * kFC) * sizeof(double) +
          (size_t)(5 * nmax + mmax) * sizeof(int);
+}
+
+#ifndef VS_FLAT_RIGID_DD
+#define VS_FLAT_RIGID_DD 16  // D_t sizes from which the D_t x D_t sums come from candidate 0 + a bound (0: off)
+#endif
+
+// Rigid-subtree mode helpers of k_flatten_dep (out of line: their registers
+// stay out of the kernel's 72).  Thread `tid`'s share (stride kFT) of
+// candidate 0's D_t x D_t filter sum.
+__device__ __noinline__ double flat_dd0_share(const double *C, int nd, int tid) {
+  double dd = 0.0;
+  int r = 0, k = tid, len = nd - 1;
+  while (r < nd - 1 && k >= len) {
+    k -= len;
+    ++r;
+    len = nd - 1 - r;
+  }
+  d3 xi{0.0, 0.0, 0.0};
+  if (r < nd - 1) xi = d3{C[(3 * r) * kFC], C[(3 * r + 1) * kFC], C[(3 * r + 2) * kFC]};
+  while (r < nd - 1) {
+    const double *q = C + 3 * (r + 1 + k) * kFC;
+    dd += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
+    k += kFT;
+    if (k >= len) {
+      do {
+        k -= len;
+        ++r;
+        len = nd - 1 - r;
+      } while (r < nd - 1 && k >= len);
+      if (r < nd - 1) xi = d3{C[(3 * r) * kFC], C[(3 * r + 1) * kFC], C[(3 * r + 2) * kFC]};
+    }
+  }
+  return dd;
+}
+
+// Lane g's share of sum_i |r_i| for candidate o: r_i = y_i(o) - (R (y_i(0) -
+// p) + p), R the rotation about torsion t's axis (stage-t endpoints, the same
+// for every candidate) by o x 10 degrees; each |r_i| taken as its 1-norm plus
+// 2^-46 X_i for the rounding of its evaluation (<= 60 u X_i).  Writes eps >=
+// ||R^T R - I||_F plus its own rounding (lane g = 0).  A degenerate axis gives
+// +inf (no exclusion).
+__device__ __noinline__ double flat_rigid_residual(const double *C, const double *Co, const double *P, int ax, int o,
+                                                   int nd, int g, double *eps) {
+  double M[12], sn, cs;
+  lattice_sc(o, sn, cs);
+  if (!torsion_setup(ld3(P + 3 * (ax & 0xffff)), ld3(P + 3 * (ax >> 16)), sn, cs, M))
+    return __longlong_as_double(0x7ff0000000000000LL);
+  const double pm = fmax(fabs(M[9]), fmax(fabs(M[10]), fabs(M[11])));
+  double rs = 0.0;
+  for (int r = g; r < nd; r += kFL) {
+    const d3 y0{C[(3 * r) * kFC], C[(3 * r + 1) * kFC], C[(3 * r + 2) * kFC]};
+    const d3 yo{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+    const d3 e = sub3(yo, torsion_apply(M, y0));
+    const double xm = fmax(fmax(fmax(fabs(y0.x), fabs(y0.y)), fmax(fabs(y0.z), fabs(yo.x))),
+                           fmax(fmax(fabs(yo.y), fabs(yo.z)), pm));
+    rs += (fabs(e.x) + fabs(e.y)) + fabs(e.z) + xm * 0x1p-46;
+  }
+  if (g == 0) {
+    double f = 0.0;
+    for (int a = 0; a < 3; ++a)
+      for (int c = a; c < 3; ++c) {
+        const double v = (M[a] * M[c] + M[3 + a] * M[3 + c]) + M[6 + a] * M[6 + c];
+        f += (a == c ? 1.0 : 2.0) * fabs(v - (a == c ? 1.0 : 0.0));
+      }
+    *eps = f + 0x1p-47;
+  }
+  return rs;
 }
 
 #ifndef VS_FLAT_ROWS
@@ -402,7 +469,9 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   double *Ms = C + 3 * nmax * kFC;  // [u][12] matrices of the candidate-independent torsions
   double *AX = Ms + 12 * mmax;      // [u][6] stage-u axis endpoints of the dependent torsions
   double *spread = AX + 6 * mmax;   // [36] filter sums A_o
-  int *dl = reinterpret_cast<int *>(spread + kFC);            // rank -> atom
+  double *devb = spread + kFC;      // [36] rigid-subtree mode: (nd - 1) * sum of residuals of candidate o
+  double *epsb = devb + kFC;        // [36] rigid-subtree mode: orthogonality defect of candidate o's map
+  int *dl = reinterpret_cast<int *>(epsb + kFC);              // rank -> atom
   int *nl = dl + nmax;                                        // common atoms, ascending
   int *slot = nl + nmax;                                      // atom -> rank, -1 for common atoms
   uint32_t *tms = reinterpret_cast<uint32_t *>(slot + nmax);  // right-set masks of the atoms
@@ -412,7 +481,8 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
   __shared__ int changed, bad, sweeps_done, s_nd, s_nn, s_ver, s_skip;
   __shared__ int stamp[VS_MAX_TORSIONS + 1];
   __shared__ uint32_t s_dt, s_du;
-  __shared__ double s_ib;
+  __shared__ double s_ib, s_dd0;
+  __shared__ int s_rig;
   const double *base = b.xyz + 3 * (size_t)a0;
   const int o = tid >> 3, g = tid & 7;
   double *Co = C + o;  // element (r, c) of this lane's candidate at Co[(3r + c) * kFC]
@@ -520,6 +590,8 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           s_dt = dt;
           s_du = du;
           s_ib = acc * (double)(nn > 0 ? nn - 1 : 0) * (1.0 + 0x1p-40);
+          s_rig = VS_FLAT_RIGID_DD > 0 && nd >= VS_FLAT_RIGID_DD;
+          s_dd0 = 0.0;
         }
       }
       __syncthreads();
@@ -617,27 +689,52 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
               }
             }
           }
-          {
-            int r = 0, k = g, len = nd - 1;
-            while (r < nd - 1 && k >= len) {
-              k -= len;
-              ++r;
-              len = nd - 1 - r;
-            }
-            d3 xi{0.0, 0.0, 0.0};
-            if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
-            while (r < nd - 1) {
-              const double *q = Co + 3 * (r + 1 + k) * kFC;
-              acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
-              k += kFL;
-              if (k >= len) {
-                do {
-                  k -= len;
-                  ++r;
-                  len = nd - 1 - r;
-                } while (r < nd - 1 && k >= len);
-                if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+          if (!s_rig) {
+            {
+              int r = 0, k = g, len = nd - 1;
+              while (r < nd - 1 && k >= len) {
+                k -= len;
+                ++r;
+                len = nd - 1 - r;
               }
+              d3 xi{0.0, 0.0, 0.0};
+              if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+              while (r < nd - 1) {
+                const double *q = Co + 3 * (r + 1 + k) * kFC;
+                acc += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
+                k += kFL;
+                if (k >= len) {
+                  do {
+                    k -= len;
+                    ++r;
+                    len = nd - 1 - r;
+                  } while (r < nd - 1 && k >= len);
+                  if (r < nd - 1) xi = d3{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
+                }
+              }
+            }
+          } else {
+            // Rigid-subtree mode.  In exact arithmetic every candidate moves
+            // D_t as one rigid body (the right subtree of t; nested axes ride
+            // along), so its D_t x D_t sum is candidate 0's: all 288 threads
+            // sum candidate 0's triangle into s_dd0, and each candidate bounds
+            // how far it is from a rigid image of candidate 0.  With y(o) =
+            // R (y(0) - p) + p + r (R: the rotation about t's axis by o x 10
+            // degrees, built here; r: the residuals),
+            //   |DD_o - DD_0| <= eps DD_0 + (nd - 1) sum_i |r_i|,
+            // eps >= the orthogonality defect of R.  D tests with these.
+            double dd = flat_dd0_share(C, nd, tid);
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, sh);
+            if (lane == 0) atomicAdd(&s_dd0, dd);
+            double eps = 0.0;
+            double rs = o != 0 ? flat_rigid_residual(C, Co, P, tax[t], o, nd, g, &eps) : 0.0;
+            rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+            rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+            rs += __shfl_xor_sync(0xffffffffu, rs, 4);
+            if (g == 0) {
+              devb[o] = rs * (double)(nd - 1) * (1.0 + 0x1p-40);
+              epsb[o] = eps;
             }
           }
           acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -655,7 +752,10 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
         int best_off = 0;
         if (!skipping) {
           // first argmax (the reference's strict > from -inf; NaN never wins)
-          const double v0 = spread[lane], v1 = lane + 32 < kFC ? spread[lane + 32] : ninf;
+          // rigid-subtree mode: A_o = spread + DD_0, and T_o lies within dev_o of it
+          const bool rig = s_rig;
+          const double dd0 = rig ? s_dd0 : 0.0;
+          const double v0 = spread[lane] + dd0, v1 = lane + 32 < kFC ? spread[lane + 32] + dd0 : ninf;
           double bv = v0 == v0 ? v0 : ninf;
           int bo = lane;
           if (v1 > bv) {
@@ -673,9 +773,13 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           }
           if (bv == ninf) bo = 0;
           const double ib2 = 2.0 * s_ib;
-          const bool n0 = lane != bo && !(bv - v0 > ((ib2 + bv + v0) * 0x1p-48 + 0x1p-499) * npairs);
+          const double ddu = dd0 * (1.0 + 0x1p-40);
+          auto dev = [&](int q) { return rig ? devb[q] + epsb[q] * ddu : 0.0; };
+          const double db = dev(bo), d0 = dev(lane), d1 = lane + 32 < kFC ? dev(lane + 32) : 0.0;
+          const bool n0 = lane != bo &&
+                          !(bv - v0 > db + d0 + ((ib2 + bv + db + v0 + d0) * 0x1p-48 + 0x1p-499) * npairs);
           const bool n1 = lane + 32 < kFC && lane + 32 != bo &&
-                          !(bv - v1 > ((ib2 + bv + v1) * 0x1p-48 + 0x1p-499) * npairs);
+                          !(bv - v1 > db + d1 + ((ib2 + bv + db + v1 + d1) * 0x1p-48 + 0x1p-499) * npairs);
           unsigned long long w = (unsigned long long)__ballot_sync(0xffffffffu, n0) |
                                  ((unsigned long long)__ballot_sync(0xffffffffu, n1) << 32);
 #ifdef VS_FLAT_FORCE_EXACT  // testing only: exact sums for every candidate
