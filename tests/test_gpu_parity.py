@@ -191,6 +191,35 @@ def test_flatten_wide_library_and_near_ties_bit_exact(gpu_ctx):
     assert np.array_equal(c1.view(np.uint64), c2.view(np.uint64)) and np.array_equal(a1, a2)
 
 
+def _flip_torsion(lig, u):
+    """The same ligand with torsion u's bond written the other way round: its
+    right set becomes the other side of the bond (the root side)."""
+    bonds = lig.bonds.copy()
+    bi = int(lig.torsion_bond[u])
+    bonds[bi] = bonds[bi][::-1]
+    rights = [r.copy() for r in lig.right_sets]
+    rights[u] = np.setdiff1d(np.arange(lig.n_atoms, dtype=np.uint16), lig.right_sets[u]).astype(np.uint16)
+    return Ligand(lig.name, lig.xyz.copy(), lig.element.copy(), lig.is_heavy.copy(), bonds, lig.bond_order.copy(),
+                  lig.torsion_bond.copy(), rights)
+
+
+def test_flatten_non_rigid_subtrees_bit_exact(gpu_ctx):
+    """k_flatten_dep's rigid-subtree mode (D_t x D_t sums taken from candidate
+    0 plus a measured residual bound) on ligands where D_t does NOT move
+    rigidly: a later torsion written root-side out makes its right set
+    straddle t's cut, the residuals are large, and the bound must send the
+    decision to the exact sums -- still bit-exact against the oracle."""
+    smi = api.synthetic_smiles(300, seed=777, heavy=(20, 50), rot=(3, 10), grammar=1)
+    raw = api.prepare_smiles(smi, mode=1, nthreads=THREADS)
+    flipped = [_flip_torsion(l, l.n_torsions - 1) for l in raw if l.n_torsions >= 3 and l.n_atoms >= 30]
+    assert len(flipped) > 100
+    b = LigandBatch(flipped)
+    c1, a1, s1 = api.flatten(b, 20, gpu_ctx)
+    c2, a2, s2 = Oracle("port").flatten(b, 20, nthreads=THREADS)
+    assert np.array_equal(s1, s2)
+    assert np.array_equal(c1.view(np.uint64), c2.view(np.uint64)) and np.array_equal(a1, a2)
+
+
 def test_local_search_random_poses_bit_exact(env):
     ctx, pocket, host, b = env
     port = Oracle("port", trig=1)
