@@ -359,6 +359,18 @@ __device__ unsigned long long g_fphase[16];  // 0-6 phases, 7 CTAs, 8 decisions,
 #else
 #define FP_MARK(k)
 #endif
+// Development bounds checks (build with -DVS_DEBUG_CHECKS): trap instead of
+// reading or writing out of range.
+#ifdef VS_DEBUG_CHECKS
+#define VS_KCHECK(c) \
+  do {               \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define VS_KCHECK(c) \
+  do {               \
+  } while (0)
+#endif
 constexpr int kFC = 36;         // candidates per torsion (10-degree lattice offsets)
 constexpr int kFL = 8;          // lanes per candidate
 constexpr int kFT = kFC * kFL;  // 288 threads = 9 full warps
@@ -397,6 +409,7 @@ __device__ __noinline__ double flat_dd0_share(const double *C, int nd, int tid) 
   d3 xi{0.0, 0.0, 0.0};
   if (r < nd - 1) xi = d3{C[(3 * r) * kFC], C[(3 * r + 1) * kFC], C[(3 * r + 2) * kFC]};
   while (r < nd - 1) {
+    VS_KCHECK(r + 1 + k < nd);
     const double *q = C + 3 * (r + 1 + k) * kFC;
     dd += dsqrt_filter(sqn3(sub3(xi, d3{q[0], q[kFC], q[2 * kFC]})));
     k += kFT;
@@ -426,6 +439,7 @@ __device__ __noinline__ double flat_rigid_residual(const double *C, const double
     return __longlong_as_double(0x7ff0000000000000LL);
   const double pm = fmax(fabs(M[9]), fmax(fabs(M[10]), fabs(M[11])));
   double rs = 0.0;
+  VS_KCHECK(o > 0 && o < kFC && nd <= VS_MAX_ATOMS);
   for (int r = g; r < nd; r += kFL) {
     const d3 y0{C[(3 * r) * kFC], C[(3 * r + 1) * kFC], C[(3 * r + 2) * kFC]};
     const d3 yo{Co[(3 * r) * kFC], Co[(3 * r + 1) * kFC], Co[(3 * r + 2) * kFC]};
@@ -1016,9 +1030,11 @@ __device__ void best_conformation(const batch_dev &b, int l, const double *hc, c
   const double *base = b.xyz + 3 * (size_t)a0;
   const uint32_t *tm = b.atom_tmask + a0;
   const uint16_t *hl = b.heavy_list + a0;
+  VS_KCHECK(m <= VS_MAX_TORSIONS && n <= N && N <= VS_MAX_ATOMS);
   if (lane == 0)
     for (int t = 0; t < m; ++t) {
       const int ia = b.tors_a[t0 + t], ib = b.tors_b[t0 + t];
+      VS_KCHECK(ia < N && ib < N);
       d3 pa = ld3(base + 3 * ia), pb = ld3(base + 3 * ib);
       const uint32_t ma = tm[ia], mb = tm[ib];
       for (int w = 0; w < t; ++w) {
@@ -1374,6 +1390,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) k_best_conf(batch_dev b, searc
   if (l >= b.n_lig) return;
   const int bidx = d.best_idx[l];
   if (bidx < 0) return;
+  VS_KCHECK(bidx < c.k);
   const int k = c.k, m = b.meta[l].m;
   const int a0 = b.atom_off[l], t0 = b.tors_off[l];
   const size_t item = (size_t)l * k + bidx;
