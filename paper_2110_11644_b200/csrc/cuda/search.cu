@@ -582,6 +582,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
 
   while (true) {  // one ligand per CTA pass
     __syncthreads();  // previous ligand finished by every warp
+    PH(22)
     if (threadIdx.x == 0) {
       sh_lig = atomicAdd(A.work, 1);
       sh_r = 0;
@@ -647,6 +648,7 @@ __global__ void __launch_bounds__(32 * kWarps, SCR ? VS_SCREEN_MINB : VS_SEARCH_
       __syncthreads();
     }
     const int J = 12 + 2 * m;
+    PH(23)
 
   while (true) {  // restarts of this ligand, one per warp at a time
     int r = 0;

@@ -33,7 +33,7 @@ def main():
     fn(buf, 1)
     r = api.dock_and_score_batch(pocket, ligs, cfg, ctx)
     fn(buf, 1)
-    tot = (sum(buf[i] for i in range(len(NAMES))) + buf[19] + buf[20] + buf[21]) or 1
+    tot = (sum(buf[i] for i in range(len(NAMES))) + buf[19] + buf[20] + buf[21] + buf[22] + buf[23]) or 1
     print(f"stage ms {r.stage_ms}")
     print(f"iterations {buf[11]}, with matrix rebuild {buf[10]} ({100.0 * buf[10] / max(buf[11], 1):.1f} %)")
     nb = max(buf[10], 1)
@@ -45,6 +45,9 @@ def main():
               f"iteration, rigid {buf[18]})")
     for i, name in enumerate(NAMES):
         print(f"{name:32s} {100.0 * buf[i] / tot:6.2f} %   {buf[i] / 1e9:10.3f} Gcycles")
+    if buf[22] + buf[23]:
+        print(f"ligand-end barrier wait (+ end of a ligand) {100.0 * buf[22] / tot:.2f} %, ligand staging + start "
+              f"matrices {100.0 * buf[23] / tot:.2f} %")
     sub = buf[19] + buf[20] + buf[21] + buf[6]
     if buf[19] + buf[20] + buf[21]:
         print("adopt torsion split (% of all): matrices + D_t heavy atoms "
