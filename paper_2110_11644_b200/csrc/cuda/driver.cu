@@ -98,7 +98,7 @@ struct vs_pocket {
   double spacing = 0.5;
   int dims[3] = {0, 0, 0};
   int n_protein = 0;
-  DevBuf values, pxyz, pclass, cell_start, cell_atoms, packed, palette, screen;
+  DevBuf values, pxyz, pclass, cell_start, cell_rec, packed, palette, screen;
   int packed_mode = 0;
   bool has_screen = false;
   vsd::screen_grid scr{};
@@ -132,7 +132,7 @@ struct vs_pocket {
     }
     p.cs = cs;
     p.cell_start = has_cells ? cell_start.as<int>() : nullptr;
-    p.cell_atoms = has_cells ? cell_atoms.as<int>() : nullptr;
+    p.cell_rec = has_cells ? reinterpret_cast<const double2 *>(cell_rec.p) : nullptr;
     p.packed.mode = packed_mode;
     p.packed.cx = bricks[0];
     p.packed.cy = bricks[1];
@@ -218,7 +218,6 @@ vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
                 .push_back(j);
         }
   }
-  (void)elem;
   std::vector<int> start(static_cast<size_t>(ncell) + 1, 0), atoms;
   for (int64_t c = 0; c < ncell; ++c) {
     start[static_cast<size_t>(c)] = static_cast<int>(atoms.size());
@@ -226,10 +225,18 @@ vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
   }
   start[static_cast<size_t>(ncell)] = static_cast<int>(atoms.size());
   if (atoms.empty()) atoms.push_back(0);
+  // the entries as records (x, y, z, class): chem_atom reads one 32-byte
+  // record per protein atom instead of an index and then the atom
+  std::vector<double> rec(4 * atoms.size());
+  for (size_t q = 0; q < atoms.size(); ++q) {
+    const int j = atoms[q];
+    for (int a = 0; a < 3; ++a) rec[4 * q + a] = xyz[3 * j + a];
+    rec[4 * q + 3] = static_cast<double>(chem_class(elem[j]));
+  }
+  CUDA_TRY(p->cell_rec.ensure(rec.size() * sizeof(double)));
+  CUDA_TRY(cudaMemcpy(p->cell_rec.p, rec.data(), rec.size() * sizeof(double), cudaMemcpyHostToDevice));
   CUDA_TRY(p->cell_start.ensure(start.size() * sizeof(int)));
-  CUDA_TRY(p->cell_atoms.ensure(atoms.size() * sizeof(int)));
   CUDA_TRY(cudaMemcpy(p->cell_start.p, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(p->cell_atoms.p, atoms.data(), atoms.size() * sizeof(int), cudaMemcpyHostToDevice));
   p->has_cells = true;
   return VS_OK;
 }

@@ -85,7 +85,7 @@ struct pocket_dev {
   double cs;                // cell size
   int cdims[3];
   const int *cell_start;    // ncells+1
-  const int *cell_atoms;
+  const double2 *cell_rec;  // per cell entry two double2: (x, y), (z, class as a double), protein order
 };
 
 struct search_cfg {
