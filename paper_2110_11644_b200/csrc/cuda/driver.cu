@@ -169,9 +169,13 @@ void ensure_lattice(int device) {
 
 int chem_class(uint8_t e) { return e == VS_ELEM_C ? 0 : ((e == VS_ELEM_N || e == VS_ELEM_O) ? 1 : 2); }
 
-// 1 A cells: 64% of the listed atoms lie within 4.5 A of a point of the cell
-// (2 A: 43%); k_select -12% against 2 A cells (measured), lists stay L2-sized
-constexpr double kChemCell = 1.0;
+// Cell edge: the smallest of these whose grid stays within kChemCellsMax
+// cells.  Smaller cells list fewer atoms beyond 4.5 A (1 A: 64% of the listed
+// atoms are within 4.5 A of a point of the cell, 2 A: 43%); measured select
+// per 131k-ligand step: 2 A +12%, 1 A 19.3 ms, 0.75 A 18.4 ms, 0.5 A 17.7 ms
+// (records: 32 B per entry, ~60 MB for the 65^3 bench pocket at 0.75 A).
+constexpr double kChemCells[] = {0.75, 1.0, 1.5, 2.0, 3.0};
+constexpr int64_t kChemCellsMax = int64_t(1) << 21;
 
 // Culling cells for chem_score: every protein atom whose distance to the
 // cell's box is below 4.5 A (+1e-6 margin), listed in protein order.
@@ -179,15 +183,25 @@ vs_status build_cells(vs_pocket *p, const uint8_t *elem, const double *xyz) {
   const double cutoff = 4.5 + 1e-6;
   // cell edge: smaller cells list fewer atoms beyond 4.5 A per cell (A/B
   // override VSDOCK_CHEM_CELL, development only)
-  double cs = kChemCell;
-  if (const char *e = std::getenv("VSDOCK_CHEM_CELL")) cs = std::atof(e) > 0.25 ? std::atof(e) : cs;
   double lo[3], hi[3];
   for (int a = 0; a < 3; ++a) {
     lo[a] = p->origin[a] - 5.0;
     hi[a] = p->origin[a] + p->spacing * (p->dims[a] - 1) + 5.0;
-    p->cdims[a] = static_cast<int>(std::ceil((hi[a] - lo[a]) / cs));
     p->cmin[a] = lo[a];
   }
+  auto cells_of = [&](double c) {
+    int64_t nc = 1;
+    for (int a = 0; a < 3; ++a) nc *= static_cast<int64_t>(std::ceil((hi[a] - lo[a]) / c));
+    return nc;
+  };
+  double cs = kChemCells[sizeof(kChemCells) / sizeof(kChemCells[0]) - 1];
+  for (const double c : kChemCells)
+    if (cells_of(c) <= kChemCellsMax) {
+      cs = c;
+      break;
+    }
+  if (const char *e = std::getenv("VSDOCK_CHEM_CELL")) cs = std::atof(e) > 0.25 ? std::atof(e) : cs;  // A/B only
+  for (int a = 0; a < 3; ++a) p->cdims[a] = static_cast<int>(std::ceil((hi[a] - lo[a]) / cs));
   p->cs = cs;
   const int64_t ncell = static_cast<int64_t>(p->cdims[0]) * p->cdims[1] * p->cdims[2];
   if (ncell <= 0 || ncell > (1 << 22) || p->n_protein == 0) {
