@@ -1249,7 +1249,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(batch_dev b, pocket_dev 
 
 // The same for k <= 32 restarts with one warp per ligand (lane = restart /
 // leader / survivor): no CTA barriers, 4 independent ligands per CTA.
-constexpr int kSelWarps = 4;
+#ifndef VS_SEL_WARPS
+#define VS_SEL_WARPS 4
+#endif
+constexpr int kSelWarps = VS_SEL_WARPS;  // ligands (warps) per select CTA
 #ifndef VS_SEL_UNROLL
 #define VS_SEL_UNROLL 8  // RMSD loads in flight (measured: 1 and 4 -> 20.6 ms, 8 -> 19.7 ms select per step)
 #endif
