@@ -6,8 +6,9 @@ Workload (BASELINE.json configs[1]): one 3CL-sized synthetic pocket
 heavy atoms), synthetic drug-like ligands (~30 heavy atoms, 5-7 rotatable
 bonds, prepared with prepare_ligand and quantised to the f32 wire format),
 30 restarts, 30 rescored.  A step docks one batch of ligands per GPU
-(default 131,072; the default 8 timed steps dock 1,048,576 ligands = the 1M
-library of configs[1]).  Multi-GPU: one process per GPU, each docks its own
+(default 262,144; the default 4 timed steps dock 1,048,576 ligands = the 1M
+library of configs[1]; measured: 262,144-ligand batches amortise the
+persistent search kernel's end-of-launch tail, +0.55% over 131,072).  Multi-GPU: one process per GPU, each docks its own
 shard (weak scaling, no data-path collective); the host top-K merge of
 merge.cpp:131-135 runs after the timed region.
 
@@ -43,10 +44,10 @@ UNIT = "ligands/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--steps", type=int, default=4)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--batch", type=int, default=131072, help="ligands per GPU per step")
+    p.add_argument("--batch", type=int, default=262144, help="ligands per GPU per step")
     p.add_argument("--restarts", type=int, default=30)
     p.add_argument("--rescored", type=int, default=30)
     p.add_argument("--seed", type=int, default=20260819)

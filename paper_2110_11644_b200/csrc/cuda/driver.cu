@@ -947,7 +947,7 @@ static vs_status dock_impl(vs_context *ctx, const vs_pocket *const *pockets, int
   ctx->last_launches = 0;
   for (double &x : ctx->stage_ms) x = 0.0;
   float total_ms = 0.0f;
-  const std::vector<int> cut = pre ? std::vector<int>{0, pre->n} : chunks(batch, k, size_t(12) << 30);
+  const std::vector<int> cut = pre ? std::vector<int>{0, pre->n} : chunks(batch, k, size_t(32) << 30);
   for (size_t ci = 0; ci + 1 < cut.size(); ++ci) {
     const int l0 = cut[ci], l1 = cut[ci + 1];
     Staged st_local;
