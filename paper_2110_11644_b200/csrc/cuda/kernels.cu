@@ -977,6 +977,9 @@ __device__ __forceinline__ int chem_class_of(uint8_t e) { return e == 0 ? 0 : ((
 #ifndef VS_CHEM_REC2
 #define VS_CHEM_REC2 1
 #endif
+#ifndef VS_CHEM_REC4
+#define VS_CHEM_REC4 0  // A/B: four records in flight
+#endif
 __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, double &total, int &clashes,
                                           int &pairs) {
   int lo = 0, hi = p.n_protein;
@@ -1008,6 +1011,18 @@ __device__ __forceinline__ void chem_atom(const pocket_dev &p, d3 x, int ci, dou
   if (culled) {
     // culled cell: 32-byte records in list order (two in flight with VS_CHEM_REC2)
     const double2 *rec = p.cell_rec;
+#if VS_CHEM_REC4
+    for (; q + 4 <= hi; q += 4) {
+      double2 a[4], bb[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[e] = __ldg(rec + 2 * (q + e));
+        bb[e] = __ldg(rec + 2 * (q + e) + 1);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pair(d3{a[e].x, a[e].y, bb[e].x}, (int)bb[e].y);
+    }
+#endif
 #if VS_CHEM_REC2
     for (; q + 2 <= hi; q += 2) {
       const double2 a0 = __ldg(rec + 2 * q), b0 = __ldg(rec + 2 * q + 1);
