@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(kFT, VS_FLAT_MINB) k_flatten_dep(batch_dev b, 
           }
           if (bv == ninf) bo = 0;
           const double ib2 = 2.0 * s_ib;
-          const double ddu = dd0 * (1.0 + 0x1p-40);
+          const double ddu = dd0 * (1.0 + 0x1p-30);  // >= the exact DD_0: filter sum + 2^-50 per distance + gamma(<= 32640 terms) < 2^-37
           auto dev = [&](int q) { return rig ? devb[q] + epsb[q] * ddu : 0.0; };
           const double db = dev(bo), d0 = dev(lane), d1 = lane + 32 < kFC ? dev(lane + 32) : 0.0;
           const bool n0 = lane != bo &&
